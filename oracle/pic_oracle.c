@@ -1,0 +1,112 @@
+/* CPU oracle for the kernelweave.pic hot path -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference PIC cycle (reference:
+ * /root/reference/pkg/src/kernelweave/pic/{kernels,particles}.py and
+ * kw/atomics.py) used by tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg as the checker and the CPU timing
+ * port.  It is never linked into, or called by, the product library.
+ *
+ * Parity: pinned bitwise against golden dumps of the unmodified reference
+ * (tests/golden/make_golden.py, tests/test_oracle_golden.py).
+ *
+ * Build: oracle/Makefile (gcc -O2 -ffp-contract=off -fopenmp).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__FP_FAST_FMA) && !defined(ORACLE_ALLOW_FMA)
+/* contraction is disabled by -ffp-contract=off; this only documents intent */
+#endif
+
+typedef struct {
+    int64_t n_sc, cap;
+    const int32_t *head, *next_f;
+    uint8_t *occ;
+    void *ox, *oy, *oz, *ux, *uy, *uz, *w;
+    void *epx, *epy, *epz, *bpx, *bpy, *bpz;
+    void *oox, *ooy, *ooz;
+    int32_t *cx, *cy, *cz, *ocx, *ocy, *ocz;
+} orc_store;
+
+typedef struct {
+    int64_t nx, ny, nz;
+    double dx, dy, dz;
+    void *Ex, *Ey, *Ez, *Bx, *By, *Bz, *Jx, *Jy, *Jz;
+} orc_fields;
+
+typedef struct {
+    int32_t *head, *tail, *next_f, *prev_f, *owner, *nfilled, *free_stack;
+    int64_t *free_top;
+} orc_pool;
+
+static inline int64_t pymod(int64_t a, int64_t n) {
+    int64_t r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+/* pic/fields.py:24-31 STAGGER, in the order Ex Ey Ez Bx By Bz. */
+static const double ORC_STAGGER[6][3] = {
+    {1.0, 0.5, 0.5}, {0.5, 1.0, 0.5}, {0.5, 0.5, 1.0},
+    {0.5, 1.0, 1.0}, {1.0, 0.5, 1.0}, {1.0, 1.0, 0.5},
+};
+
+int orc_version(void) { return 1; }
+
+#define FT float
+#define SFX _f32
+#include "pic_oracle_impl.h"
+#undef FT
+#undef SFX
+
+#define FT double
+#define SFX _f64
+#include "pic_oracle_impl.h"
+#undef FT
+#undef SFX
+
+/* pic/particles.py:214-235 `_scan_leavers`: canonical order (super cell
+ * ascending, chain order, slot ascending). */
+int64_t orc_scan_leavers(const orc_store *st, const int32_t *nfilled, int64_t scx, int64_t scy,
+                         int64_t scz, int64_t gx, int64_t gy, int32_t *out_f, int32_t *out_s,
+                         int32_t *out_dest) {
+    int64_t n = 0;
+    for (int64_t sc = 0; sc < st->n_sc; ++sc) {
+        for (int32_t f = st->head[sc]; f >= 0; f = st->next_f[f]) {
+            if (nfilled[f] <= 0) continue;
+            for (int64_t s = 0; s < st->cap; ++s) {
+                int64_t q = (int64_t)f * st->cap + s;
+                if (!st->occ[q]) continue;
+                int64_t dsc = (st->cx[q] / scx) + gx * ((st->cy[q] / scy) + gy * (st->cz[q] / scz));
+                if (dsc != sc) {
+                    out_f[n] = f;
+                    out_s[n] = (int32_t)s;
+                    out_dest[n] = (int32_t)dsc;
+                    ++n;
+                }
+            }
+        }
+    }
+    return n;
+}
+
+/* pic/particles.py:290-313 `_unlink_empty`. */
+void orc_unlink_empty(orc_pool *pl, int64_t n_sc) {
+    for (int64_t sc = 0; sc < n_sc; ++sc) {
+        int32_t f = pl->head[sc];
+        while (f >= 0) {
+            int32_t nxt = pl->next_f[f];
+            if (pl->nfilled[f] == 0) {
+                int32_t p = pl->prev_f[f], q = pl->next_f[f];
+                if (p >= 0) pl->next_f[p] = q; else pl->head[sc] = q;
+                if (q >= 0) pl->prev_f[q] = p; else pl->tail[sc] = p;
+                pl->owner[f] = -1;
+                pl->next_f[f] = -1;
+                pl->prev_f[f] = -1;
+                pl->free_stack[pl->free_top[0]] = f;
+                pl->free_top[0] += 1;
+            }
+            f = nxt;
+        }
+    }
+}
