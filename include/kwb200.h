@@ -1,0 +1,163 @@
+/* kwb200 -- B200-native PIC cycle behind a plain C ABI.
+ *
+ * The drop-in boundary for the kernelweave.pic hot path
+ * (reference: /root/reference/pkg/src/kernelweave/pic/sim.py:134-176,
+ * Simulation.step).  Each entry point replaces one or more stage kernel
+ * objects the reference launches through kw/kernel.py:232 `launch()`:
+ *
+ *   kwb_particles_advance  <- GatherKernel + PushKernel + MoveKernel +
+ *                             DepositKernel (+ ATOMICS.add_dense)
+ *                             pic/kernels.py:341-412, kw/atomics.py:147-163
+ *   kwb_particles_shift    <- migrate_particles   pic/particles.py:316-345
+ *   kwb_fields_faraday_half<- FaradayHalfKernel   pic/kernels.py:415-431
+ *   kwb_fields_ampere      <- AmpereKernel        pic/kernels.py:434-450
+ *   kwb_charge_density     <- Simulation.charge_density / _rho_tsc
+ *                             pic/sim.py:183-189, pic/kernels.py:291-326
+ *   kwb_continuity_residual<- the validate block  pic/sim.py:168-175
+ *   kwb_particle_moments / kwb_field_stats
+ *                          <- Simulation.diagnostics pic/sim.py:191-225
+ *   kwb_store_load / kwb_store_export
+ *                          <- _bulk_fill / SuperCellStore.packed
+ *                             pic/sim.py:305-328, pic/particles.py:174-186
+ *
+ * Conventions
+ *  - All device memory is owned by the caller (PyTorch tensors); the library
+ *    never allocates.  Pointers are device pointers.
+ *  - Every call is asynchronous on `stream` and returns 0 on success or a
+ *    negative KWB_E* code; kwb_last_error() gives the message (thread-local).
+ *  - Field arrays: logical (nx, ny, nz), stored x fastest:
+ *    index = (k * ny + j) * nx + i.  Periodic in x, y and z.
+ *  - Particle stores: one per species, super cell s owns slots
+ *    [s * slots_per_sc, s * slots_per_sc + count[s]) (dense); a slot holds
+ *    the in-cell offsets, momentum u = gamma v, weight, and the local cell
+ *    index lx + scx * (ly + scy * lz) within the super cell.
+ *  - Super-cell index s = bx + gx * (by + gy * bz) (pic/sim.py:79-84).
+ *  - dtype KWB_F32 / KWB_F64 selects the storage type F; arithmetic follows
+ *    the reference's mixed-precision recipe with no
+ *    FMA contraction, so particle results are bitwise equal to the reference.
+ */
+#ifndef KWB200_H
+#define KWB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KWB_VERSION 1
+
+#define KWB_F32 0
+#define KWB_F64 1
+
+#define KWB_OK 0
+#define KWB_EINVAL (-1)
+#define KWB_ECUDA (-2)
+
+/* status words written by the device (int32 array of KWB_STATUS_WORDS) */
+#define KWB_ST_MOVE_ERRORS 0   /* particles that moved >= 1 cell (ContractViolation) */
+#define KWB_ST_EXCH_OVERFLOW 1 /* leavers that did not fit the exchange buffer */
+#define KWB_ST_STORE_OVERFLOW 2/* arrivals that did not fit their super cell */
+#define KWB_ST_LEAVERS 3       /* leavers summed over species this step */
+#define KWB_ST_MAX_COUNT 4     /* max particles in one super cell after the shift */
+#define KWB_ST_LOAD_ERRORS 5   /* kwb_store_load records outside their super cell */
+#define KWB_STATUS_WORDS 8
+
+typedef struct CUstream_st *kwb_stream_t;
+
+typedef struct kwb_grid {
+    int32_t nx, ny, nz;    /* cells */
+    int32_t scx, scy, scz; /* super cell (frame capacity = scx*scy*scz) */
+    int32_t gx, gy, gz;    /* super-cell grid = cells / super cell */
+    int32_t dtype;         /* KWB_F32 or KWB_F64 */
+    double dx, dy, dz, dt;
+} kwb_grid;
+
+typedef struct kwb_species {
+    double qm_half_dt; /* q dt / (2 m)             pic/sim.py:101-103 */
+    double fac[3];     /* -q delta_a / (dt V)      pic/sim.py:104-110 */
+    double dt_d[3];    /* dt / delta_a             pic/sim.py:100 */
+    double q_inv_vol;  /* q / V                    pic/sim.py:188 */
+    double charge, mass;
+} kwb_species;
+
+typedef struct kwb_store {
+    void *ox, *oy, *oz;   /* F: in-cell offsets in [0, 1] */
+    void *ux, *uy, *uz;   /* F: momentum gamma v (units of c) */
+    void *w;              /* F: macro-particle weight */
+    uint16_t *cell;       /* local cell index within the super cell */
+    int32_t *count;       /* [n_sc] particles per super cell */
+    int32_t slots_per_sc; /* frames_per_sc * frame capacity */
+} kwb_store;
+
+typedef struct kwb_exchange {
+    void *ox, *oy, *oz, *ux, *uy, *uz, *w; /* F[capacity] */
+    int32_t *cx, *cy, *cz;                 /* global cell after the move */
+    int32_t *dest;                         /* destination super cell */
+    int32_t *count;                        /* [1] device counter, zeroed by advance */
+    int32_t capacity;
+} kwb_exchange;
+
+int kwb_version(void);
+const char *kwb_last_error(void);
+
+/* Fused gather -> Boris push -> move -> Esirkepov deposit for one species.
+ * Reads store `in`, writes staying particles densely into `out` and leavers
+ * into `ex`; accumulates current into J (which the caller zeroes once per
+ * step).  shape_order: 1 CIC, 2 TSC (reference), 3 PCS. */
+int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
+                          const kwb_store *out, const kwb_exchange *ex,
+                          void *const E[3], void *const B[3], void *const J[3],
+                          int shape_order, int32_t *status, kwb_stream_t stream);
+
+/* Super-cell shift: append the leavers in `ex` to their destination super
+ * cells of `out` (restores "every particle lives in its owning super cell"). */
+int kwb_particles_shift(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,
+                        int32_t *status, kwb_stream_t stream);
+
+/* Yee updates (in place). */
+int kwb_fields_faraday_half(const kwb_grid *g, void *const E[3], void *const B[3],
+                            double half_dt, kwb_stream_t stream);
+int kwb_fields_ampere(const kwb_grid *g, void *const E[3], void *const B[3],
+                      void *const J[3], double dt, kwb_stream_t stream);
+
+/* Validation charge density (float64, accumulated, caller zeroes rho). */
+int kwb_charge_density(const kwb_grid *g, const kwb_species *sp, const kwb_store *st,
+                       int shape_order, double *rho, kwb_stream_t stream);
+
+/* out[0] = max |(rho_new - rho_prev)/dt + div J| (div J in storage type,
+ * as numpy computes it, pic/fields.py:154-160); out[1] = max |G - G_prev|
+ * with G = div E - rho_new (G_prev updated in place; pass NULL to skip). */
+int kwb_continuity_residual(const kwb_grid *g, const double *rho_new, const double *rho_prev,
+                            void *const J[3], void *const E[3], double *G_prev,
+                            double *out, kwb_stream_t stream);
+
+/* out[0] += census, out[1] += sum q w, out[2] += sum m (gamma-1) w (float64). */
+int kwb_particle_moments(const kwb_grid *g, const kwb_species *sp, const kwb_store *st,
+                         double *out, kwb_stream_t stream);
+
+/* out[0] = sum over cells of E^2 + B^2 (float64), out[1] = max |div B|. */
+int kwb_field_stats(const kwb_grid *g, void *const E[3], void *const B[3], double *out,
+                    kwb_stream_t stream);
+
+/* Load canonical-order records (sorted by super cell; sc_start[n_sc+1]
+ * offsets) into an empty store; global cells cx/cy/cz, F arrays. */
+int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n, const int64_t *sc_start,
+                   const int32_t *cx, const int32_t *cy, const int32_t *cz,
+                   void *const f7[7], int32_t *status, kwb_stream_t stream);
+
+/* Export to canonical super-cell order; out_start[n_sc] = exclusive scan of
+ * count.  Writes global cells and the 7 F arrays. */
+int kwb_store_export(const kwb_grid *g, const kwb_store *st, const int64_t *out_start,
+                     int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
+                     kwb_stream_t stream);
+
+/* Copy each super cell's dense range into a store with a different
+ * slots_per_sc (capacity growth). */
+int kwb_store_repack(const kwb_grid *g, const kwb_store *src, const kwb_store *dst,
+                     kwb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KWB200_H */

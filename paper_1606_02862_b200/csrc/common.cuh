@@ -1,0 +1,131 @@
+// Shared device helpers for libkwb200 (sm_100a).
+//
+// The whole library is compiled with --fmad=false: the reference kernels
+// (Numba/LLVM, no fast-math) never contract a*b+c, so neither may we if the
+// particle state is to stay bitwise equal.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kwb200.h"
+
+namespace kwb {
+
+constexpr int kThreads = 256;  // one CTA per super cell, 8 warps
+
+// Python floor-mod (non-negative for n > 0).
+__host__ __device__ __forceinline__ int pymod(int a, int n) {
+    int r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+// Field index for the x-fastest layout: (k * ny + j) * nx + i.
+__device__ __forceinline__ int64_t fidx(int i, int j, int k, int nx, int ny) {
+    return ((int64_t)k * ny + j) * nx + i;
+}
+
+template <typename F>
+struct StoreT {
+    F *ox, *oy, *oz, *ux, *uy, *uz, *w;
+    uint16_t *cell;
+    int32_t *count;
+    int32_t slots;
+};
+
+template <typename F>
+__host__ inline StoreT<F> store_of(const kwb_store &s) {
+    StoreT<F> t;
+    t.ox = (F *)s.ox; t.oy = (F *)s.oy; t.oz = (F *)s.oz;
+    t.ux = (F *)s.ux; t.uy = (F *)s.uy; t.uz = (F *)s.uz;
+    t.w = (F *)s.w;
+    t.cell = s.cell;
+    t.count = s.count;
+    t.slots = s.slots_per_sc;
+    return t;
+}
+
+template <typename F>
+struct ExchT {
+    F *ox, *oy, *oz, *ux, *uy, *uz, *w;
+    int32_t *cx, *cy, *cz, *dest, *count;
+    int32_t capacity;
+};
+
+template <typename F>
+__host__ inline ExchT<F> exch_of(const kwb_exchange &e) {
+    ExchT<F> t;
+    t.ox = (F *)e.ox; t.oy = (F *)e.oy; t.oz = (F *)e.oz;
+    t.ux = (F *)e.ux; t.uy = (F *)e.uy; t.uz = (F *)e.uz;
+    t.w = (F *)e.w;
+    t.cx = e.cx; t.cy = e.cy; t.cz = e.cz; t.dest = e.dest; t.count = e.count;
+    t.capacity = e.capacity;
+    return t;
+}
+
+struct Geo {
+    int nx, ny, nz, scx, scy, scz, gx, gy, gz;
+    double dx, dy, dz, dt;
+};
+
+__host__ inline Geo geo_of(const kwb_grid &g) {
+    Geo o;
+    o.nx = g.nx; o.ny = g.ny; o.nz = g.nz;
+    o.scx = g.scx; o.scy = g.scy; o.scz = g.scz;
+    o.gx = g.gx; o.gy = g.gy; o.gz = g.gz;
+    o.dx = g.dx; o.dy = g.dy; o.dz = g.dz; o.dt = g.dt;
+    return o;
+}
+
+// Atomic max on a non-negative double via its bit pattern.
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
+    atomicMax((unsigned long long *)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// Shape orders: 1 CIC, 2 TSC (reference), 3 PCS.  NP = support array length,
+// H = tile halo (and array centre offset).
+template <int ORDER>
+struct Shape {
+    static constexpr int NP = (ORDER == 3) ? 7 : 5;
+    static constexpr int H = (ORDER == 3) ? 3 : 2;
+};
+
+// pic/kernels.py:138-150 `_shape5_into` (TSC) and the CIC/PCS extension
+// (SURVEY.md §8c): out[idx] = (F) W(|x - ((idx - H) + 0.5)|).
+template <typename F, int ORDER>
+__device__ __forceinline__ void shape_into(double x, F (&out)[Shape<ORDER>::NP]) {
+    constexpr int NP = Shape<ORDER>::NP, H = Shape<ORDER>::H;
+#pragma unroll
+    for (int idx = 0; idx < NP; ++idx) {
+        double d = x - ((double)(idx - H) + 0.5);
+        if (d < 0) d = -d;
+        double v;
+        if (ORDER == 2) {
+            if (d < 0.5) v = 0.75 - d * d;
+            else if (d < 1.5) { double e = 1.5 - d; v = (0.5 * e) * e; }
+            else v = 0.0;
+        } else if (ORDER == 1) {
+            v = (d < 1.0) ? 1.0 - d : 0.0;
+        } else {
+            if (d < 1.0) v = ((4.0 - (6.0 * d) * d) + ((3.0 * d) * d) * d) / 6.0;
+            else if (d < 2.0) { double e = 2.0 - d; v = ((e * e) * e) / 6.0; }
+            else v = 0.0;
+        }
+        out[idx] = (F)v;
+    }
+}
+
+// Transverse factor, pic/kernels.py:215-218, evaluated left to right:
+// ((F(a0*b0) + (0.5*da)*b0) + (0.5*a0)*db) + F(da*db)/3.0
+template <typename F>
+__device__ __forceinline__ double transverse(F a0, F da, F b0, F db) {
+    F p00 = a0 * b0, pdd = da * db;
+    return (((double)p00 + (0.5 * (double)da) * (double)b0) + (0.5 * (double)a0) * (double)db) +
+           (double)pdd / 3.0;
+}
+
+}  // namespace kwb
+
+// thread-local error text for kwb_last_error()
+void kwb_set_error(const char *fmt, ...);
+int kwb_check_launch(const char *what);

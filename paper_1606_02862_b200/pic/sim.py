@@ -1,0 +1,410 @@
+"""The PIC cycle on B200 (API of kernelweave.pic.sim, reference
+pic/sim.py:33-328).
+
+``Simulation.step()`` runs, on one CUDA stream and with no host round trip
+inside the cycle:
+
+    J = 0
+    per species:  kwb_particles_advance  (gather -> push -> move -> deposit,
+                                          compaction into the spare columns)
+                  kwb_particles_shift    (leavers into their new super cell)
+    kwb_fields_faraday_half -> kwb_fields_ampere -> kwb_fields_faraday_half
+    [validate]    kwb_charge_density + kwb_continuity_residual (+ Gauss drift)
+
+then reads one small status word block (move violations, capacity) and
+raises ``ContractViolation`` exactly where the reference's DepositKernel
+would (pic/kernels.py:405-408).  The reference's order -- all species
+deposit, then migrate, then the field update -- is preserved.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from .. import _lib
+from ..backend import B200Backend
+from ..errors import AllocationError, CapabilityError, ContractViolation
+from ..workdiv import make_work_division
+from .fields import ALL_COMPONENTS, YeeFieldSet, div_b, div_j, field_energy  # noqa: F401
+from .params import SimParams, default_species  # noqa: F401
+from .particles import SuperCellStore
+
+STRATEGIES = ("elements", "threads")
+EXCHANGE_FRACTION = 0.25
+
+
+def _near_cubic_factors(n: int) -> tuple[int, int, int]:
+    """Deterministic balanced factorisation (pic/sim.py:36-52)."""
+    best, best_score = (n, 1, 1), n
+    for px in range(1, n + 1):
+        if n % px:
+            continue
+        rest = n // px
+        for py in range(1, rest + 1):
+            if rest % py:
+                continue
+            pz = rest // py
+            score = max(px, py, pz) - min(px, py, pz)
+            if score < best_score:
+                best_score, best = score, (px, py, pz)
+    return best
+
+
+def _grid_struct(p: SimParams) -> _lib.Grid:
+    g = _lib.Grid()
+    g.nx, g.ny, g.nz = p.cells.as_tuple()
+    g.scx, g.scy, g.scz = p.super_cell.as_tuple()
+    g.gx, g.gy, g.gz = p.super_cell_grid.as_tuple()
+    g.dtype = _lib.KWB_F32 if p.dtype == np.float32 else _lib.KWB_F64
+    g.dx, g.dy, g.dz, g.dt = p.dx, p.dy, p.dz, p.dt
+    return g
+
+
+def _species_struct(p: SimParams, s) -> _lib.SpeciesC:
+    c = _lib.SpeciesC()
+    deltas = (p.dx, p.dy, p.dz)
+    vol = p.cell_volume
+    c.qm_half_dt = s.charge * p.dt / (2.0 * s.mass)            # pic/sim.py:101-103
+    for a in range(3):
+        c.fac[a] = -s.charge * deltas[a] / (p.dt * vol)       # pic/sim.py:104-110
+        c.dt_d[a] = p.dt / deltas[a]                           # pic/sim.py:100
+    c.q_inv_vol = s.charge / vol                               # pic/sim.py:188
+    c.charge, c.mass = s.charge, s.mass
+    return c
+
+
+class _Exchange:
+    """Leaver buffer shared by the species of one Simulation."""
+
+    def __init__(self, capacity, tdtype, device):
+        self.capacity = int(capacity)
+        for c in ("ox", "oy", "oz", "ux", "uy", "uz", "w"):
+            setattr(self, c, torch.empty(self.capacity, dtype=tdtype, device=device))
+        for c in ("cx", "cy", "cz", "dest"):
+            setattr(self, c, torch.empty(self.capacity, dtype=torch.int32, device=device))
+        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+        e = _lib.ExchangeC()
+        for c in ("ox", "oy", "oz", "ux", "uy", "uz", "w", "cx", "cy", "cz", "dest", "count"):
+            setattr(e, c, getattr(self, c).data_ptr())
+        e.capacity = self.capacity
+        self.cstruct = e
+
+
+class Simulation:
+    """Fields + per-species super-cell stores, stepped on one B200."""
+
+    def __init__(self, params: SimParams, backend=None, strategy="elements", validate=True):
+        if strategy not in STRATEGIES:
+            raise ValueError(f"strategy must be one of {STRATEGIES}")
+        if backend is None:
+            backend = B200Backend()
+        if not isinstance(backend, B200Backend):
+            raise CapabilityError(
+                f"{type(backend).__name__} is not supported: this build runs the PIC cycle "
+                "on a B200 only (no CPU back-end, no fallback)")
+        _lib.load()
+        self.params = params
+        self.backend = backend
+        self.device = backend.device
+        self.strategy = strategy
+        self.validate = validate
+        self.step_count = 0
+        p = params
+        self.shape_order = p.shape_order
+        self.fields = YeeFieldSet(p.cells, p.dx, p.dy, p.dz, p.dtype, self.device)
+        self.stores = [SuperCellStore(p.cells, p.super_cell, p.dtype, self.device)
+                       for _ in p.species]
+        grid = p.super_cell_grid
+        n_sc = grid.volume
+        sc = p.super_cell.as_tuple()
+        s = np.arange(n_sc)
+        self.origins = np.stack([(s % grid.x) * sc[0], ((s // grid.x) % grid.y) * sc[1],
+                                 (s // (grid.x * grid.y)) * sc[2]], axis=1).astype(np.int64)
+        hw = 3 if self.shape_order == 3 else 2
+        cells = p.cells.as_tuple()
+        # wrapped deposit-tile -> grid maps (pic/sim.py:88-94; halo 3 for PCS)
+        self.maps = tuple(((self.origins[:, a:a + 1] - hw + np.arange(sc[a] + 2 * hw)[None, :])
+                           % cells[a]).astype(np.int64) for a in range(3))
+        self.tile_shape = tuple(sc[a] + 2 * hw for a in range(3))
+        self._grid = _grid_struct(p)
+        self._species = [_species_struct(p, sp) for sp in p.species]
+        self._status = torch.zeros((len(p.species), _lib.STATUS_WORDS), dtype=torch.int32,
+                                   device=self.device)
+        self._status_host = torch.zeros_like(self._status, device="cpu").pin_memory()
+        self._exchange = None
+        self._rho_prev = None
+        self._G_prev = None
+        self._resid = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self._wd = None
+
+    # -- launch plumbing ------------------------------------------------------
+    def work_division(self):
+        """Descriptive: one block per super cell (the CUDA mapping is fixed)."""
+        if self._wd is None:
+            grid, sc = self.params.super_cell_grid, self.params.super_cell
+            if self.strategy == "elements":
+                self._wd = make_work_division(grid, (1, 1, 1), sc)
+            else:
+                self._wd = make_work_division(grid, sc, (1, 1, 1))
+        return self._wd
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _E(self):
+        return _lib.ptr3([self.fields.storage(n) for n in ("Ex", "Ey", "Ez")])
+
+    def _B(self):
+        return _lib.ptr3([self.fields.storage(n) for n in ("Bx", "By", "Bz")])
+
+    def _J(self):
+        return _lib.ptr3([self.fields.storage(n) for n in ("Jx", "Jy", "Jz")])
+
+    def _exchange_buffer(self) -> _Exchange:
+        need = max(st.slots_per_sc * st.n_super_cells for st in self.stores)
+        cap = int(math.ceil(EXCHANGE_FRACTION * need)) + 65536
+        if self._exchange is None or self._exchange.capacity < min(cap, need + 65536):
+            self._exchange = _Exchange(min(cap, need + 65536), self.stores[0].tdtype, self.device)
+        return self._exchange
+
+    # -- the PIC cycle ------------------------------------------------------
+    def step(self):
+        self.enqueue_step()
+        self.check_status()
+
+    def enqueue_step(self):
+        """Launch one full PIC cycle on the current stream (no host sync)."""
+        f = self.fields
+        stream = self._stream()
+        g = ctypes.byref(self._grid)
+        if self.validate and self._rho_prev is None:
+            self._rho_prev = self._charge_density_storage()
+            self._G_prev = torch.zeros_like(self._rho_prev)
+            _lib.call("kwb_continuity_residual", g, self._rho_prev.data_ptr(), None, self._J(),
+                      self._E(), self._G_prev.data_ptr(), self._resid.data_ptr(), stream)
+        f.zero_current()
+        self._status.zero_()
+        E, B, J = self._E(), self._B(), self._J()
+        ex = self._exchange_buffer()
+        for i, st in enumerate(self.stores):
+            src, dst = st.current, st.spare()
+            _lib.call("kwb_particles_advance", g, ctypes.byref(self._species[i]),
+                      ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
+                      ctypes.byref(ex.cstruct), E, B, J, self.shape_order,
+                      self._status[i].data_ptr(), stream)
+            _lib.call("kwb_particles_shift", g, ctypes.byref(dst.cstruct()),
+                      ctypes.byref(ex.cstruct), self._status[i].data_ptr(), stream)
+            st.swap()
+        self.update_fields()
+        if self.validate:
+            rho_new = self._charge_density_storage()
+            _lib.call("kwb_continuity_residual", g, rho_new.data_ptr(), self._rho_prev.data_ptr(),
+                      J, E, self._G_prev.data_ptr(), self._resid.data_ptr(), stream)
+            self._rho_prev = rho_new
+        self.step_count += 1
+
+    def update_fields(self):
+        """Yee leapfrog B(1/2) -> E -> B(1/2) with the current J
+        (pic/sim.py:164-167)."""
+        p = self.params
+        g, stream = ctypes.byref(self._grid), self._stream()
+        E, B, J = self._E(), self._B(), self._J()
+        _lib.call("kwb_fields_faraday_half", g, E, B, p.dt / 2.0, stream)
+        _lib.call("kwb_fields_ampere", g, E, B, J, p.dt, stream)
+        _lib.call("kwb_fields_faraday_half", g, E, B, p.dt / 2.0, stream)
+
+    def load_state(self, fields=None, particles=None):
+        """Replace fields (name -> (nx, ny, nz) array) and/or particles (one
+        dict of canonical records per species: global cx cy cz, ox oy oz,
+        ux uy uz, w).  Used for restart and teacher-forced parity runs."""
+        if fields:
+            for n, a in fields.items():
+                self.fields.load_numpy(n, a)
+        if particles is not None:
+            if len(particles) != len(self.stores):
+                raise ValueError("one particle dict per species expected")
+            for st, arrays in zip(self.stores, particles):
+                st.load_packed(arrays)
+        self._rho_prev = None
+        self._G_prev = None
+
+    def check_status(self):
+        """Read the device status words (one small D2H) and raise on any
+        contract or capacity violation; grow stores that run full."""
+        self._status_host.copy_(self._status, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        st = self._status_host
+        moved = int(st[:, _lib.ST_MOVE_ERRORS].sum())
+        if moved:
+            raise ContractViolation(
+                f"{moved} particle(s) moved a full cell or more before deposit")
+        lost = int(st[:, _lib.ST_EXCH_OVERFLOW].sum() + st[:, _lib.ST_STORE_OVERFLOW].sum())
+        if lost:
+            raise AllocationError(
+                f"{lost} particle(s) did not fit the exchange buffer or their super cell "
+                "this step; raise EXCHANGE_FRACTION / HEADROOM")
+        for i, store in enumerate(self.stores):
+            store.reserve(int(st[i, _lib.ST_MAX_COUNT]))
+        return st.clone()
+
+    def run(self, steps: int):
+        for _ in range(steps):
+            self.step()
+
+    @property
+    def last_residual(self) -> float:
+        return float(self._resid[0].item()) if self.step_count else 0.0
+
+    @property
+    def last_gauss_drift(self) -> float:
+        """max |G^{n+1} - G^n|, G = div E - rho (validate=True only)."""
+        return float(self._resid[1].item()) if self.step_count else 0.0
+
+    # -- validation / diagnostics ---------------------------------------------
+    def _charge_density_storage(self) -> torch.Tensor:
+        nx, ny, nz = self.params.cells.as_tuple()
+        rho = torch.zeros((nz, ny, nx), dtype=torch.float64, device=self.device)
+        g = ctypes.byref(self._grid)
+        for i, st in enumerate(self.stores):
+            _lib.call("kwb_charge_density", g, ctypes.byref(self._species[i]),
+                      ctypes.byref(st.current.cstruct()), self.shape_order, rho.data_ptr(),
+                      self._stream())
+        return rho
+
+    def charge_density(self) -> torch.Tensor:
+        """float64 charge density, logical (nx, ny, nz) view (pic/sim.py:183-189)."""
+        return self._charge_density_storage().permute(2, 1, 0)
+
+    def _moments(self) -> np.ndarray:
+        out = torch.zeros((len(self.stores), 3), dtype=torch.float64, device=self.device)
+        g = ctypes.byref(self._grid)
+        for i, st in enumerate(self.stores):
+            _lib.call("kwb_particle_moments", g, ctypes.byref(self._species[i]),
+                      ctypes.byref(st.current.cstruct()), out[i].data_ptr(), self._stream())
+        return out.cpu().numpy()
+
+    def census(self) -> int:
+        return sum(st.census() for st in self.stores)
+
+    def kinetic_energy(self) -> float:
+        return float(self._moments()[:, 2].sum())
+
+    def total_charge(self) -> float:
+        return float(self._moments()[:, 1].sum())
+
+    def diagnostics(self) -> dict:
+        m = self._moments()
+        s, max_div_b = field_stats(self.fields)
+        f = self.fields
+        return {
+            "total_charge": float(m[:, 1].sum()),
+            "field_energy": 0.5 * s * f.dx * f.dy * f.dz,
+            "kinetic_energy": float(m[:, 2].sum()),
+            "max_div_b": max_div_b,
+            "max_continuity_residual": self.last_residual,
+        }
+
+    def total_energy(self) -> float:
+        return field_energy(self.fields) + self.kinetic_energy()
+
+
+def field_stats(fields: YeeFieldSet):
+    """(sum of E^2 + B^2, max |div B|) via kwb_field_stats."""
+    g = _lib.Grid()
+    g.nx, g.ny, g.nz = fields.cells.as_tuple()
+    g.scx = g.scy = g.scz = 1
+    g.gx, g.gy, g.gz = g.nx, g.ny, g.nz
+    g.dtype = _lib.KWB_F32 if fields.dtype == np.float32 else _lib.KWB_F64
+    g.dx, g.dy, g.dz, g.dt = fields.dx, fields.dy, fields.dz, 1.0
+    out = torch.zeros(2, dtype=torch.float64, device=fields.device)
+    E = _lib.ptr3([fields.storage(n) for n in ("Ex", "Ey", "Ez")])
+    B = _lib.ptr3([fields.storage(n) for n in ("Bx", "By", "Bz")])
+    _lib.call("kwb_field_stats", ctypes.byref(g), E, B, out.data_ptr(),
+              torch.cuda.current_stream(fields.device).cuda_stream)
+    o = out.cpu().numpy()
+    return float(o[0]), float(o[1])
+
+
+def diagnostics(sim: Simulation) -> dict:
+    return sim.diagnostics()
+
+
+def step(sim: Simulation) -> None:
+    sim.step()
+
+
+def khi_species_particles(params: SimParams, seed: int, sp_i: int, sc_begin: int = 0,
+                          sc_end: int | None = None, rng=None):
+    """init_khi's particle generation for super cells [sc_begin, sc_end) of
+    one species, vectorised (pic/sim.py:239-302).  Returns float64 offsets and
+    momenta and int64 global cells, in generation (canonical) order.  Pass the
+    same ``rng`` across consecutive chunks to continue the species stream."""
+    p = params
+    ppc = p.particles_per_cell
+    px, py, pz = _near_cubic_factors(ppc)
+    sub = np.stack([
+        np.tile((np.arange(px) + 0.5) / px, py * pz),
+        np.tile(np.repeat((np.arange(py) + 0.5) / py, px), pz),
+        np.repeat((np.arange(pz) + 0.5) / pz, px * py),
+    ], axis=1)
+    scx, scy, scz = p.super_cell.as_tuple()
+    grid = p.super_cell_grid
+    gx, gy = grid.x, grid.y
+    cap = p.frame_capacity
+    sc_end = grid.volume if sc_end is None else sc_end
+    scs = np.arange(sc_begin, sc_end)
+    nsc = scs.shape[0]
+    s = np.arange(cap)
+    loc = np.stack([s % scx, (s // scx) % scy, s // (scx * scy)], axis=1).astype(np.int64)
+    org = np.stack([(scs % gx) * scx, ((scs // gx) % gy) * scy, (scs // (gx * gy)) * scz], axis=1)
+    cxyz = org[:, None, :] + loc[None, :, :]
+    cx = np.repeat(cxyz[:, :, 0], ppc, axis=1).reshape(-1)
+    cy = np.repeat(cxyz[:, :, 1], ppc, axis=1).reshape(-1)
+    cz = np.repeat(cxyz[:, :, 2], ppc, axis=1).reshape(-1)
+    n_per_sc = cap * ppc
+    ox = np.tile(sub[:, 0], cap * nsc)
+    oy = np.tile(sub[:, 1], cap * nsc)
+    oz = np.tile(sub[:, 2], cap * nsc)
+    x_abs = (cx + ox) * p.dx
+    v0, amp = p.stream_velocity, p.perturbation
+    vx = np.where(cy < p.cells.y // 2, v0, -v0)
+    vy = amp * np.sin(2.0 * math.pi * x_abs / (p.cells.x * p.dx))
+    vz = np.zeros_like(vx)
+    gam = 1.0 / np.sqrt(1.0 - (vx * vx + vy * vy + vz * vz))
+    ux, uy, uz = vx * gam, vy * gam, vz * gam
+    if p.thermal_u > 0:
+        if rng is None:
+            rng = np.random.default_rng((seed, sp_i))
+        z = rng.normal(0.0, p.thermal_u, 3 * n_per_sc * nsc).reshape(nsc, 3, n_per_sc)
+        ux = ux + z[:, 0, :].reshape(-1)
+        uy = uy + z[:, 1, :].reshape(-1)
+        uz = uz + z[:, 2, :].reshape(-1)
+    return dict(cx=cx, cy=cy, cz=cz, ox=ox, oy=oy, oz=oz, ux=ux, uy=uy, uz=uz)
+
+
+def init_khi(params: SimParams, seed: int = 0, backend=None, strategy="elements",
+             validate=True, chunk_super_cells: int = 4096) -> Simulation:
+    """Kelvin-Helmholtz setup (pic/sim.py:239-302): counter-streaming layers
+    split along y, sinusoidal v_y perturbation, quiet-start placement,
+    thermal jitter from default_rng((seed, species_index)); E = B = 0.
+    Generated on the host in the reference's exact draw order (bitwise the
+    same initial state), then uploaded into the device stores."""
+    sim = Simulation(params, backend=backend, strategy=strategy, validate=validate)
+    p = params
+    n_sc = p.super_cell_grid.volume
+    dt = p.dtype
+    for sp_i, (species, store) in enumerate(zip(p.species, sim.stores)):
+        rng = np.random.default_rng((seed, sp_i)) if p.thermal_u > 0 else None
+        parts = []
+        for b in range(0, n_sc, chunk_super_cells):
+            a = khi_species_particles(p, seed, sp_i, b, min(n_sc, b + chunk_super_cells), rng)
+            parts.append({k: (v.astype(np.int32) if k in ("cx", "cy", "cz") else v.astype(dt))
+                          for k, v in a.items()})
+        arrays = {k: np.concatenate([q[k] for q in parts]) for k in parts[0]}
+        arrays["w"] = np.full(arrays["cx"].shape, species.weight, dtype=dt)
+        store.load_packed(arrays, presorted=True)
+    return sim
