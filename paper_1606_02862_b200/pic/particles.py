@@ -214,33 +214,32 @@ class SuperCellStore:
         cx/cy/cz plus ox oy oz ux uy uz w).  Records are grouped by super
         cell (stable), capacity is sized with headroom, and the load kernel
         writes them into the dense segments."""
-        cx = np.asarray(arrays["cx"], dtype=np.int64)
-        cy = np.asarray(arrays["cy"], dtype=np.int64)
-        cz = np.asarray(arrays["cz"], dtype=np.int64)
-        n = cx.shape[0]
+        def up(a, tdt):
+            t = torch.as_tensor(np.asarray(a)) if not isinstance(a, torch.Tensor) else a
+            return t.to(device=self.device, dtype=tdt, non_blocking=True).contiguous()
+
+        d_cells = [up(arrays[c], torch.int32) for c in ("cx", "cy", "cz")]
+        d_f = [up(arrays[c], self.tdtype) for c in FLOAT_COLUMNS]
+        n = d_cells[0].shape[0]
         scx, scy, scz = self.super_cell.as_tuple()
         gx, gy, _ = self.sc_grid.as_tuple()
+        cx, cy, cz = (c.to(torch.int64) for c in d_cells)
+        if n:
+            lo = torch.stack([cx.min(), cy.min(), cz.min()]).cpu()
+            hi = torch.stack([cx.max(), cy.max(), cz.max()]).cpu()
+            if int(lo.min()) < 0 or any(int(hi[a]) >= self.cells.as_tuple()[a] for a in range(3)):
+                raise ContractViolation("particle cell index outside the grid")
         sc = (cx // scx) + gx * ((cy // scy) + gy * (cz // scz))
-        if n and (cx.min() < 0 or cy.min() < 0 or cz.min() < 0 or cx.max() >= self.cells.x
-                  or cy.max() >= self.cells.y or cz.max() >= self.cells.z):
-            raise ContractViolation("particle cell index outside the grid")
-        order = None if presorted else np.argsort(sc, kind="stable")
-        counts = np.bincount(sc, minlength=self.n_super_cells)
-        self.frames_per_sc = max(1, math.ceil(int(counts.max(initial=0)) * HEADROOM
-                                              / self.capacity) + 1)
+        if not presorted and n:
+            sc, order = torch.sort(sc, stable=True)
+            d_cells = [c[order] for c in d_cells]
+            d_f = [c[order] for c in d_f]
+        counts = torch.bincount(sc, minlength=self.n_super_cells)
+        max_count = int(counts.max().item()) if n else 0
+        self.frames_per_sc = max(1, math.ceil(max_count * HEADROOM / self.capacity) + 1)
         self._cols = [self._new_columns(), None]
-        start = np.zeros(self.n_super_cells + 1, dtype=np.int64)
-        np.cumsum(counts, out=start[1:])
-
-        def up(a, dt):
-            a = np.asarray(a)
-            if order is not None:
-                a = a[order]
-            return torch.from_numpy(np.ascontiguousarray(a.astype(dt, copy=False))).to(self.device)
-
-        d_cells = [up(c, np.int32) for c in (cx, cy, cz)]
-        d_f = [up(arrays[c], self.dtype) for c in FLOAT_COLUMNS]
-        d_start = torch.from_numpy(start).to(self.device)
+        d_start = torch.zeros(self.n_super_cells + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(counts, 0, out=d_start[1:])
         status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)
         g = self._grid_struct()
         _lib.call("kwb_store_load", _lib.ctypes.byref(g), _lib.ctypes.byref(self.current.cstruct()),
