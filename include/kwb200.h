@@ -27,10 +27,16 @@
  *    negative KWB_E* code; kwb_last_error() gives the message (thread-local).
  *  - Field arrays: logical (nx, ny, nz), stored x fastest:
  *    index = (k * ny + j) * nx + i.  Periodic in x, y and z.
- *  - Particle stores: one per species, super cell s owns slots
- *    [s * slots_per_sc, s * slots_per_sc + count[s]) (dense); a slot holds
- *    the in-cell offsets, momentum u = gamma v, weight, and the local cell
- *    index lx + scx * (ly + scy * lz) within the super cell.
+ *  - Particle stores ("cell-column frames"): one per species.  With
+ *    V = scx*scy*scz cells per super cell (= the frame capacity) and K
+ *    frames per super cell, slot (s, k, c) = (s * K + k) * V + c holds the
+ *    k-th particle of local cell c = lx + scx * (ly + scy * lz) of super
+ *    cell s.  Column (s, c) is filled in frames [0, front) and [K-back, K);
+ *    the cell of a particle is implied by its column.  A frame therefore
+ *    holds one particle of every cell, so a warp reading frame k of 32
+ *    adjacent cells issues fully coalesced 128-byte loads, and the thread
+ *    that owns cell c sees only particles of cell c (register-resident
+ *    current deposit).
  *  - Super-cell index s = bx + gx * (by + gy * bz) (pic/sim.py:79-84).
  *  - dtype KWB_F32 / KWB_F64 selects the storage type F; arithmetic follows
  *    the reference's mixed-precision recipe with no
@@ -59,8 +65,8 @@ extern "C" {
 #define KWB_ST_EXCH_OVERFLOW 1 /* leavers that did not fit the exchange buffer */
 #define KWB_ST_STORE_OVERFLOW 2/* arrivals that did not fit their super cell */
 #define KWB_ST_LEAVERS 3       /* leavers summed over species this step */
-#define KWB_ST_MAX_COUNT 4     /* max particles in one super cell after the shift */
-#define KWB_ST_LOAD_ERRORS 5   /* kwb_store_load records outside their super cell */
+#define KWB_ST_MAX_COUNT 4     /* max particles in one cell column after the shift */
+#define KWB_ST_LOAD_ERRORS 5   /* kwb_store_load records that did not fit */
 #define KWB_STATUS_WORDS 8
 
 typedef struct CUstream_st *kwb_stream_t;
@@ -85,9 +91,9 @@ typedef struct kwb_store {
     void *ox, *oy, *oz;   /* F: in-cell offsets in [0, 1] */
     void *ux, *uy, *uz;   /* F: momentum gamma v (units of c) */
     void *w;              /* F: macro-particle weight */
-    uint16_t *cell;       /* local cell index within the super cell */
-    int32_t *count;       /* [n_sc] particles per super cell */
-    int32_t slots_per_sc; /* frames_per_sc * frame capacity */
+    int32_t *front;       /* [n_sc * V] column fill from frame 0 upward */
+    int32_t *back;        /* [n_sc * V] column fill from frame K-1 downward */
+    int32_t frames_per_sc;/* K: frames per super cell */
 } kwb_store;
 
 typedef struct kwb_exchange {
@@ -102,16 +108,19 @@ int kwb_version(void);
 const char *kwb_last_error(void);
 
 /* Fused gather -> Boris push -> move -> Esirkepov deposit for one species.
- * Reads store `in`, writes staying particles densely into `out` and leavers
- * into `ex`; accumulates current into J (which the caller zeroes once per
- * step).  shape_order: 1 CIC, 2 TSC (reference), 3 PCS. */
+ * One CTA per super cell, one thread per cell.  Reads store `in`; writes
+ * particles that stay in their cell to the front of the same column of
+ * `out`, particles that change cell inside the super cell to the back of
+ * their new column, and leavers of the super cell into `ex`.  Accumulates
+ * current into J (which the caller zeroes once per step).
+ * shape_order: 1 CIC, 2 TSC (reference), 3 PCS. */
 int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex,
                           void *const E[3], void *const B[3], void *const J[3],
                           int shape_order, int32_t *status, kwb_stream_t stream);
 
-/* Super-cell shift: append the leavers in `ex` to their destination super
- * cells of `out` (restores "every particle lives in its owning super cell"). */
+/* Super-cell shift: append the leavers in `ex` to the back of their new
+ * columns in `out` (restores "every particle lives in its owning super cell"). */
 int kwb_particles_shift(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,
                         int32_t *status, kwb_stream_t stream);
 
@@ -140,20 +149,21 @@ int kwb_particle_moments(const kwb_grid *g, const kwb_species *sp, const kwb_sto
 int kwb_field_stats(const kwb_grid *g, void *const E[3], void *const B[3], double *out,
                     kwb_stream_t stream);
 
-/* Load canonical-order records (sorted by super cell; sc_start[n_sc+1]
- * offsets) into an empty store; global cells cx/cy/cz, F arrays. */
-int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n, const int64_t *sc_start,
+/* Append n particle records (global cells cx/cy/cz, 7 F arrays, any order)
+ * to their columns; front/back must be valid (zero for an empty store). */
+int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
                    const int32_t *cx, const int32_t *cy, const int32_t *cz,
                    void *const f7[7], int32_t *status, kwb_stream_t stream);
 
-/* Export to canonical super-cell order; out_start[n_sc] = exclusive scan of
- * count.  Writes global cells and the 7 F arrays. */
-int kwb_store_export(const kwb_grid *g, const kwb_store *st, const int64_t *out_start,
+/* Export in canonical order (super cell, then local cell, then frame):
+ * cell_start[n_sc * V] = exclusive scan of front + back per column.
+ * Writes global cells and the 7 F arrays. */
+int kwb_store_export(const kwb_grid *g, const kwb_store *st, const int64_t *cell_start,
                      int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
                      kwb_stream_t stream);
 
-/* Copy each super cell's dense range into a store with a different
- * slots_per_sc (capacity growth). */
+/* Copy every column into a store with a different frames_per_sc
+ * (capacity growth). */
 int kwb_store_repack(const kwb_grid *g, const kwb_store *src, const kwb_store *dst,
                      kwb_stream_t stream);
 

@@ -40,7 +40,7 @@ class SpeciesC(ctypes.Structure):
 
 class StoreC(ctypes.Structure):
     _fields_ = [("ox", P), ("oy", P), ("oz", P), ("ux", P), ("uy", P), ("uz", P),
-                ("w", P), ("cell", P), ("count", P), ("slots_per_sc", I32)]
+                ("w", P), ("front", P), ("back", P), ("frames_per_sc", I32)]
 
 
 class ExchangeC(ctypes.Structure):
@@ -64,7 +64,7 @@ _SIGS = {
     "kwb_continuity_residual": ([P, P, P, Ptr3, Ptr3, P, P, P], ctypes.c_int),
     "kwb_particle_moments": ([P, P, P, P, P], ctypes.c_int),
     "kwb_field_stats": ([P, Ptr3, Ptr3, P, P], ctypes.c_int),
-    "kwb_store_load": ([P, P, I64, P, P, P, P, Ptr7, P, P], ctypes.c_int),
+    "kwb_store_load": ([P, P, I64, P, P, P, Ptr7, P, P], ctypes.c_int),
     "kwb_store_export": ([P, P, P, P, P, P, Ptr7, P], ctypes.c_int),
     "kwb_store_repack": ([P, P, P, P], ctypes.c_int),
 }

@@ -28,9 +28,8 @@ __device__ __forceinline__ int64_t fidx(int i, int j, int k, int nx, int ny) {
 template <typename F>
 struct StoreT {
     F *ox, *oy, *oz, *ux, *uy, *uz, *w;
-    uint16_t *cell;
-    int32_t *count;
-    int32_t slots;
+    int32_t *front, *back;
+    int32_t frames;
 };
 
 template <typename F>
@@ -39,9 +38,9 @@ __host__ inline StoreT<F> store_of(const kwb_store &s) {
     t.ox = (F *)s.ox; t.oy = (F *)s.oy; t.oz = (F *)s.oz;
     t.ux = (F *)s.ux; t.uy = (F *)s.uy; t.uz = (F *)s.uz;
     t.w = (F *)s.w;
-    t.cell = s.cell;
-    t.count = s.count;
-    t.slots = s.slots_per_sc;
+    t.front = s.front;
+    t.back = s.back;
+    t.frames = s.frames_per_sc;
     return t;
 }
 

@@ -1,25 +1,31 @@
 """Super-cell/frame particle store in HBM (API of kernelweave.pic.particles,
 reference pic/particles.py:35-211).
 
-Layout (B200-first, not the reference's linked lists): every super cell owns
-``frames_per_sc`` frames of ``frame capacity`` (= super-cell volume = 256)
-slots, contiguous in HBM, and keeps its particles DENSE in slots
-[0, count[sc]).  Frame ``k`` of super cell ``s`` is global frame
-``s * frames_per_sc + k``; frames past ceil(count/capacity) are free.  So
+Layout -- "cell-column frames" (B200-first, not the reference's linked
+lists).  A super cell of V cells (V = frame capacity = 256 by default) owns
+K frames of V slots.  Frame k holds the k-th particle of EVERY cell of the
+super cell: slot (s, k, c) = (s*K + k)*V + c.  Column (s, c) -- the
+particles of local cell c -- fills frames [0, front) from the bottom and
+[K-back, K) from the top.  Consequences:
 
-* there are no occupancy masks, holes, chain links or free stacks: the
-  reference's ``grow(count)`` pool overshoot (5-32x) and fragmentation
-  (occupancy 0.38-0.47 after 100 steps) cannot happen;
-* each SoA column (ox oy oz ux uy uz w: storage type; cell: 16-bit local
-  cell index) is read and written with fully coalesced 128-byte warp
-  transactions, one CTA per super cell;
-* two copies of the columns alternate every step: the fused advance kernel
-  reads one and writes the compacted survivors into the other, so the
-  super-cell shift costs no extra pass over the particles.
+* the particle's cell is implied by its column: no per-particle cell index
+  and no occupancy mask are stored (28 B/particle in fp32);
+* a warp reading frame k of 32 adjacent cells issues one fully coalesced
+  128-B transaction per SoA column;
+* the CUDA thread that owns cell c sees only particles of cell c, so the
+  Esirkepov current of non-crossing particles accumulates in registers;
+* no holes, free stacks or pool overshoot: the reference's ``grow(count)``
+  reserves a free frame per leaver (5-32x over-allocation);
+  here K only has to exceed the fullest cell.
 
-Capacity grows (repack) when a super cell passes 85% of its slots.
-The reference's canonical order is preserved at super-cell granularity;
-slot order within a super cell may differ.
+Two copies of the columns alternate every step: the advance kernel reads one
+and writes the other (stayers to the front of their column, in-super-cell
+movers to the back of their new column), the shift kernel appends arrivals
+from other super cells to the back.  K grows (repack) when a column passes
+85% of it.  Canonical order (export/packed) is super cell, then local cell,
+then frame; the reference orders by frame chain and slot within a super
+cell, so comparisons are order-independent within a super cell (SURVEY.md
+§8b).
 """
 
 from __future__ import annotations
@@ -37,34 +43,33 @@ from .pusher import MacroParticle
 
 FLOAT_COLUMNS = ("ox", "oy", "oz", "ux", "uy", "uz", "w")
 PACKED_FIELDS = ("cx", "cy", "cz", "ox", "oy", "oz", "ux", "uy", "uz", "w")
-HEADROOM = 1.25
+HEADROOM = 1.3
 GROW_AT = 0.85
 
 
 class _Columns:
-    __slots__ = ("ox", "oy", "oz", "ux", "uy", "uz", "w", "cell", "count", "slots")
+    __slots__ = ("ox", "oy", "oz", "ux", "uy", "uz", "w", "front", "back", "frames")
 
-    def __init__(self, n_sc, slots, tdtype, device):
-        n = n_sc * slots
+    def __init__(self, n_sc, cells, frames, tdtype, device):
+        n = n_sc * frames * cells
         for c in FLOAT_COLUMNS:
             setattr(self, c, torch.zeros(n, dtype=tdtype, device=device))
-        self.cell = torch.zeros(n, dtype=torch.int16, device=device)
-        self.count = torch.zeros(n_sc, dtype=torch.int32, device=device)
-        self.slots = slots
+        self.front = torch.zeros(n_sc * cells, dtype=torch.int32, device=device)
+        self.back = torch.zeros(n_sc * cells, dtype=torch.int32, device=device)
+        self.frames = frames
 
     def cstruct(self) -> _lib.StoreC:
         s = _lib.StoreC()
-        for c in FLOAT_COLUMNS + ("cell", "count"):
+        for c in FLOAT_COLUMNS + ("front", "back"):
             setattr(s, c, getattr(self, c).data_ptr())
-        s.slots_per_sc = self.slots
+        s.frames_per_sc = self.frames
         return s
 
 
 class SuperCellStore:
-    """Per-species particle store: dense super-cell segments of frames."""
+    """Per-species particle store: cell-column frames per super cell."""
 
-    def __init__(self, cells, super_cell, dtype=np.float64, device="cuda",
-                 frames_per_sc: int = 1):
+    def __init__(self, cells, super_cell, dtype=np.float64, device="cuda", frames_per_sc: int = 4):
         self.cells = Extent3.of(cells)
         self.super_cell = Extent3.of(super_cell)
         self.sc_grid = Extent3(self.cells.x // self.super_cell.x,
@@ -72,21 +77,20 @@ class SuperCellStore:
                                self.cells.z // self.super_cell.z)
         self.n_super_cells = self.sc_grid.volume
         self.capacity = self.super_cell.volume
-        if self.capacity > 65535:
-            raise ContractViolation("super-cell volume must fit a 16-bit local cell index")
+        if self.capacity > 256:
+            raise ContractViolation(
+                f"super-cell volume {self.capacity} > 256: one CUDA thread owns one cell")
         self.dtype = np.dtype(dtype)
         self.tdtype = TORCH_DTYPE[self.dtype]
         self.device = torch.device(device)
         self.frames_per_sc = max(1, int(frames_per_sc))
         self._cols = [self._new_columns(), None]
+        self.loaded = 0  # particles at the last load (sizes exchange buffers without a sync)
 
     # -- storage --------------------------------------------------------------
-    @property
-    def slots_per_sc(self) -> int:
-        return self.frames_per_sc * self.capacity
-
     def _new_columns(self) -> _Columns:
-        return _Columns(self.n_super_cells, self.slots_per_sc, self.tdtype, self.device)
+        return _Columns(self.n_super_cells, self.capacity, self.frames_per_sc, self.tdtype,
+                        self.device)
 
     @property
     def current(self) -> _Columns:
@@ -94,21 +98,20 @@ class SuperCellStore:
 
     def spare(self) -> _Columns:
         """The write target of the next advance (allocated on first use)."""
-        if self._cols[1] is None or self._cols[1].slots != self.slots_per_sc:
+        if self._cols[1] is None or self._cols[1].frames != self.frames_per_sc:
             self._cols[1] = self._new_columns()
         return self._cols[1]
 
     def swap(self) -> None:
         self._cols.reverse()
 
-    def reserve(self, max_count: int, stream=None) -> bool:
-        """Grow frames_per_sc so max_count sits below GROW_AT of the slots.
-        Repacks the live particles on the device; returns True if it grew."""
-        if max_count <= GROW_AT * self.slots_per_sc:
+    def reserve(self, max_column: int, stream=None) -> bool:
+        """Grow frames_per_sc so the fullest column sits below GROW_AT of it;
+        repacks the live particles on the device.  Returns True if it grew."""
+        if max_column <= GROW_AT * self.frames_per_sc:
             return False
-        need = math.ceil(max_count * HEADROOM / self.capacity) + 1
         old = self.current
-        self.frames_per_sc = max(need, self.frames_per_sc + 1)
+        self.frames_per_sc = max(math.ceil(max_column * HEADROOM) + 4, self.frames_per_sc + 1)
         new = self._new_columns()
         g = self._grid_struct()
         _lib.call("kwb_store_repack", _lib.ctypes.byref(g), _lib.ctypes.byref(old.cstruct()),
@@ -141,30 +144,37 @@ class SuperCellStore:
     uy = property(lambda self: self._col2d("uy"))
     uz = property(lambda self: self._col2d("uz"))
     w = property(lambda self: self._col2d("w"))
-    cell = property(lambda self: self._col2d("cell"))
+
+    @property
+    def column_counts(self) -> torch.Tensor:
+        """Particles per cell column, (n_super_cells, capacity) int32."""
+        c = self.current
+        return (c.front + c.back).view(self.n_super_cells, self.capacity)
 
     @property
     def count(self) -> torch.Tensor:
         """Particles per super cell (device int32)."""
-        return self.current.count
-
-    @property
-    def nfilled(self) -> torch.Tensor:
-        """Particles per frame (n_frames,), as the reference's nfilled."""
-        cnt = self.count.to(torch.int64).view(-1, 1)
-        k = torch.arange(self.frames_per_sc, device=self.device).view(1, -1)
-        return (cnt - k * self.capacity).clamp(0, self.capacity).to(torch.int32).view(-1)
+        return self.column_counts.sum(dim=1, dtype=torch.int32)
 
     @property
     def occ(self) -> torch.Tensor:
         """Slot occupancy (n_frames, capacity) uint8, as the reference's occ."""
-        slot = torch.arange(self.slots_per_sc, device=self.device).view(1, -1)
-        m = slot < self.count.view(-1, 1)
-        return m.to(torch.uint8).view(self.n_frames, self.capacity)
+        c = self.current
+        K, V = self.frames_per_sc, self.capacity
+        k = torch.arange(K, device=self.device).view(1, K, 1)
+        f = c.front.view(-1, 1, V)
+        b = c.back.view(-1, 1, V)
+        m = (k < f) | (k >= K - b)
+        return m.to(torch.uint8).view(self.n_frames, V)
+
+    @property
+    def nfilled(self) -> torch.Tensor:
+        """Particles per frame (n_frames,), as the reference's nfilled."""
+        return self.occ.sum(dim=1, dtype=torch.int32)
 
     @property
     def owner(self) -> torch.Tensor:
-        """Owning super cell per frame, -1 for free frames."""
+        """Owning super cell per frame, -1 for empty frames."""
         sc = torch.arange(self.n_super_cells, device=self.device, dtype=torch.int32)
         own = sc.repeat_interleave(self.frames_per_sc)
         return torch.where(self.nfilled > 0, own, torch.full_like(own, -1))
@@ -175,27 +185,27 @@ class SuperCellStore:
         return linearize_3d(sc, self.sc_grid)
 
     def frames_of(self, sc: int):
-        """Frame indices of one super cell in order (its non-empty frames)."""
-        n = int(self.count[sc].item())
-        k = (n + self.capacity - 1) // self.capacity
-        return [sc * self.frames_per_sc + i for i in range(k)]
+        """Frame indices of one super cell that hold particles, in order."""
+        nf = self.nfilled[sc * self.frames_per_sc:(sc + 1) * self.frames_per_sc].cpu().numpy()
+        return [sc * self.frames_per_sc + k for k in range(self.frames_per_sc) if nf[k] > 0]
 
     def census(self) -> int:
-        return int(self.count.sum().item())
+        c = self.current
+        return int((c.front.sum(dtype=torch.int64) + c.back.sum(dtype=torch.int64)).item())
 
     def super_cell_counts(self) -> np.ndarray:
         return self.count.cpu().numpy().astype(np.int64)
 
     # -- host <-> device ------------------------------------------------------------
     def packed(self, fields=PACKED_FIELDS, stream=None) -> dict:
-        """Canonical super-cell order records as host numpy arrays (global
-        cells int32, storage-type floats), via the export kernel."""
+        """Canonical-order records (super cell, cell, frame) as host numpy
+        arrays: global cells int32, storage-type floats (export kernel)."""
         out = self.packed_device(stream)
         return {n: out[n].cpu().numpy() for n in fields}
 
     def packed_device(self, stream=None) -> dict:
-        cnt = self.count.to(torch.int64)
-        start = torch.zeros(self.n_super_cells + 1, dtype=torch.int64, device=self.device)
+        cnt = (self.current.front + self.current.back).to(torch.int64)
+        start = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=self.device)
         torch.cumsum(cnt, 0, out=start[1:])
         n = int(start[-1].item())
         out = {c: torch.empty(n, dtype=torch.int32, device=self.device) for c in ("cx", "cy", "cz")}
@@ -211,67 +221,74 @@ class SuperCellStore:
 
     def load_packed(self, arrays: dict, stream=None, presorted: bool = False) -> None:
         """Replace the store's content with particle records (global cells
-        cx/cy/cz plus ox oy oz ux uy uz w).  Records are grouped by super
-        cell (stable), capacity is sized with headroom, and the load kernel
-        writes them into the dense segments."""
+        cx/cy/cz plus ox oy oz ux uy uz w; host numpy or device tensors).
+        Columns are sized from the fullest cell with headroom; the load
+        kernel appends every record to its column."""
+        del presorted  # any order is accepted
+
         def up(a, tdt):
-            t = torch.as_tensor(np.asarray(a)) if not isinstance(a, torch.Tensor) else a
+            t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
             return t.to(device=self.device, dtype=tdt, non_blocking=True).contiguous()
 
         d_cells = [up(arrays[c], torch.int32) for c in ("cx", "cy", "cz")]
         d_f = [up(arrays[c], self.tdtype) for c in FLOAT_COLUMNS]
         n = d_cells[0].shape[0]
-        scx, scy, scz = self.super_cell.as_tuple()
-        gx, gy, _ = self.sc_grid.as_tuple()
-        cx, cy, cz = (c.to(torch.int64) for c in d_cells)
+        nx, ny, nz = self.cells.as_tuple()
+        max_col = 0
         if n:
-            lo = torch.stack([cx.min(), cy.min(), cz.min()]).cpu()
-            hi = torch.stack([cx.max(), cy.max(), cz.max()]).cpu()
-            if int(lo.min()) < 0 or any(int(hi[a]) >= self.cells.as_tuple()[a] for a in range(3)):
+            cx, cy, cz = (c.to(torch.int64) for c in d_cells)
+            lo = torch.stack([cx.min(), cy.min(), cz.min()])
+            hi = torch.stack([cx.max() - nx, cy.max() - ny, cz.max() - nz])
+            if int(lo.min().item()) < 0 or int(hi.max().item()) >= 0:
                 raise ContractViolation("particle cell index outside the grid")
-        sc = (cx // scx) + gx * ((cy // scy) + gy * (cz // scz))
-        if not presorted and n:
-            sc, order = torch.sort(sc, stable=True)
-            d_cells = [c[order] for c in d_cells]
-            d_f = [c[order] for c in d_f]
-        counts = torch.bincount(sc, minlength=self.n_super_cells)
-        max_count = int(counts.max().item()) if n else 0
-        self.frames_per_sc = max(1, math.ceil(max_count * HEADROOM / self.capacity) + 1)
+            cell = (cz * ny + cy) * nx + cx
+            max_col = int(torch.bincount(cell, minlength=nx * ny * nz).max().item())
+        self.frames_per_sc = max(8, math.ceil(max_col * HEADROOM) + 4)
+        self.loaded = n
         self._cols = [self._new_columns(), None]
-        d_start = torch.zeros(self.n_super_cells + 1, dtype=torch.int64, device=self.device)
-        torch.cumsum(counts, 0, out=d_start[1:])
         status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)
         g = self._grid_struct()
         _lib.call("kwb_store_load", _lib.ctypes.byref(g), _lib.ctypes.byref(self.current.cstruct()),
-                  n, d_start.data_ptr(), d_cells[0].data_ptr(), d_cells[1].data_ptr(),
-                  d_cells[2].data_ptr(), _lib.ptr7(d_f), status.data_ptr(),
-                  _stream(stream, self.device))
+                  n, d_cells[0].data_ptr(), d_cells[1].data_ptr(), d_cells[2].data_ptr(),
+                  _lib.ptr7(d_f), status.data_ptr(), _stream(stream, self.device))
         bad = int(status[_lib.ST_LOAD_ERRORS].item())
         if bad:
             raise AllocationError(f"{bad} particle record(s) could not be loaded")
 
     def insert(self, p: MacroParticle) -> None:
-        """Append one particle into its owning super cell (host-side path,
+        """Append one particle to its cell column (host-side path,
         pic/particles.py:129-144)."""
-        pk = self.packed()
-        for k, v in zip(("cx", "cy", "cz"), p.cell):
-            pk[k] = np.append(pk[k], np.int32(v))
-        for k, v in zip(("ox", "oy", "oz"), p.offset):
-            pk[k] = np.append(pk[k], v)
-        for k, v in zip(("ux", "uy", "uz"), p.u):
-            pk[k] = np.append(pk[k], v)
-        pk["w"] = np.append(pk["w"], p.weight)
-        self.load_packed(pk)
+        cnt = int(self.column_counts.max().item())
+        self.reserve(cnt + 1)
+        rec = {"cx": [p.cell[0]], "cy": [p.cell[1]], "cz": [p.cell[2]],
+               "ox": [p.offset[0]], "oy": [p.offset[1]], "oz": [p.offset[2]],
+               "ux": [p.u[0]], "uy": [p.u[1]], "uz": [p.u[2]], "w": [p.weight]}
+        d_cells = [torch.tensor(rec[c], dtype=torch.int32, device=self.device)
+                   for c in ("cx", "cy", "cz")]
+        d_f = [torch.tensor(rec[c], dtype=self.tdtype, device=self.device) for c in FLOAT_COLUMNS]
+        status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)
+        g = self._grid_struct()
+        _lib.call("kwb_store_load", _lib.ctypes.byref(g), _lib.ctypes.byref(self.current.cstruct()),
+                  1, d_cells[0].data_ptr(), d_cells[1].data_ptr(), d_cells[2].data_ptr(),
+                  _lib.ptr7(d_f), status.data_ptr(), _stream(None, self.device))
+        if int(status[_lib.ST_LOAD_ERRORS].item()):
+            raise AllocationError("insert: particle could not be stored")
+        self.loaded += 1
 
     def iter_particles(self):
-        """(sc, frame, slot, MacroParticle) in canonical super-cell order."""
+        """(sc, frame, slot, MacroParticle) in canonical order."""
         pk = self.packed()
-        cnt = self.super_cell_counts()
+        c = self.current
+        front = c.front.cpu().numpy()
+        back = c.back.cpu().numpy()
+        K, V = self.frames_per_sc, self.capacity
         i = 0
-        for sc in range(self.n_super_cells):
-            for s in range(int(cnt[sc])):
-                f = sc * self.frames_per_sc + s // self.capacity
-                yield sc, f, s % self.capacity, MacroParticle(
+        for col in range(front.shape[0]):
+            s, cell = divmod(col, V)
+            f, b = int(front[col]), int(back[col])
+            for j in range(f + b):
+                k = j if j < f else K - b + (j - f)
+                yield s, s * K + k, cell, MacroParticle(
                     (int(pk["cx"][i]), int(pk["cy"][i]), int(pk["cz"][i])),
                     (float(pk["ox"][i]), float(pk["oy"][i]), float(pk["oz"][i])),
                     (float(pk["ux"][i]), float(pk["uy"][i]), float(pk["uz"][i])),
@@ -279,16 +296,14 @@ class SuperCellStore:
                 i += 1
 
     def check_integrity(self):
-        """Every particle sits in its owning super cell; counts fit the frames
-        (the reference's chain/ownership/occupancy checks, pic/particles.py
-        :188-211, restated for the dense layout)."""
-        cnt = self.count
-        assert int(cnt.min().item()) >= 0, "negative super-cell count"
-        assert int(cnt.max().item()) <= self.slots_per_sc, "super cell overflows its frames"
-        occ = self.occ.view(-1).bool()
-        cells = self.current.cell.to(torch.int32)
-        assert bool(((cells >= 0) & (cells < self.capacity))[occ].all().item()), \
-            "particle outside owning super cell"
+        """Columns fit their frames and do not overlap; occupancy sums to the
+        census (the reference's chain/ownership/occupancy checks,
+        pic/particles.py:188-211, restated for the column layout; membership
+        is structural: a particle's cell is its column)."""
+        c = self.current
+        assert int(c.front.min().item()) >= 0 and int(c.back.min().item()) >= 0
+        assert int((c.front + c.back).max().item()) <= self.frames_per_sc, "column overflow"
+        assert int(self.occ.sum().item()) == self.census(), "occupancy != census"
         return True
 
 

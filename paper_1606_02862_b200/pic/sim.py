@@ -165,7 +165,7 @@ class Simulation:
         return _lib.ptr3([self.fields.storage(n) for n in ("Jx", "Jy", "Jz")])
 
     def _exchange_buffer(self) -> _Exchange:
-        need = max(st.slots_per_sc * st.n_super_cells for st in self.stores)
+        need = max(st.loaded for st in self.stores)
         cap = int(math.ceil(EXCHANGE_FRACTION * need)) + 65536
         if self._exchange is None or self._exchange.capacity < min(cap, need + 65536):
             self._exchange = _Exchange(min(cap, need + 65536), self.stores[0].tdtype, self.device)
@@ -173,20 +173,51 @@ class Simulation:
 
     # -- the PIC cycle ------------------------------------------------------
     def step(self):
-        self.enqueue_step()
+        """One PIC cycle with the reference's synchronous semantics: raises
+        ContractViolation before the field update if a particle moved a full
+        cell (pic/kernels.py:405-408).  If a cell column or the exchange
+        buffer ran full, the particle phase is undone (its input columns are
+        intact -- the advance is double-buffered), capacity grows, and the
+        phase is redone, so no particle is ever lost."""
+        self._begin_step()
+        for _attempt in range(6):
+            self._enqueue_particles()
+            st = self._read_status()
+            lost = st[:, _lib.ST_EXCH_OVERFLOW].sum() + st[:, _lib.ST_STORE_OVERFLOW].sum()
+            if int(lost) == 0:
+                break
+            self._undo_particles(st)
+        else:
+            raise AllocationError("particle phase keeps overflowing its capacity")
+        moved = int(st[:, _lib.ST_MOVE_ERRORS].sum())
+        if moved:
+            raise ContractViolation(
+                f"{moved} particle(s) moved a full cell or more before deposit")
+        self._enqueue_fields()
+        self.step_count += 1
         self.check_status()
 
     def enqueue_step(self):
-        """Launch one full PIC cycle on the current stream (no host sync)."""
-        f = self.fields
-        stream = self._stream()
-        g = ctypes.byref(self._grid)
+        """Launch one full PIC cycle on the current stream with no host sync
+        (bench / CUDA-graph path).  Capacity and contract violations are
+        reported by the next check_status(), which raises."""
+        self._begin_step()
+        self._enqueue_particles()
+        self._enqueue_fields()
+        self.step_count += 1
+
+    def _begin_step(self):
         if self.validate and self._rho_prev is None:
             self._rho_prev = self._charge_density_storage()
             self._G_prev = torch.zeros_like(self._rho_prev)
-            _lib.call("kwb_continuity_residual", g, self._rho_prev.data_ptr(), None, self._J(),
-                      self._E(), self._G_prev.data_ptr(), self._resid.data_ptr(), stream)
-        f.zero_current()
+            _lib.call("kwb_continuity_residual", ctypes.byref(self._grid),
+                      self._rho_prev.data_ptr(), None, self._J(), self._E(),
+                      self._G_prev.data_ptr(), self._resid.data_ptr(), self._stream())
+
+    def _enqueue_particles(self):
+        stream = self._stream()
+        g = ctypes.byref(self._grid)
+        self.fields.zero_current()
         self._status.zero_()
         E, B, J = self._E(), self._B(), self._J()
         ex = self._exchange_buffer()
@@ -199,13 +230,30 @@ class Simulation:
             _lib.call("kwb_particles_shift", g, ctypes.byref(dst.cstruct()),
                       ctypes.byref(ex.cstruct), self._status[i].data_ptr(), stream)
             st.swap()
+
+    def _undo_particles(self, st):
+        """Restore the pre-advance columns and grow what overflowed."""
+        for i, store in enumerate(self.stores):
+            store.swap()
+            if int(st[i, _lib.ST_STORE_OVERFLOW]):
+                store.reserve(store.frames_per_sc + int(st[i, _lib.ST_STORE_OVERFLOW]) + 4)
+        if int(st[:, _lib.ST_EXCH_OVERFLOW].sum()):
+            cap = self._exchange.capacity * 2
+            self._exchange = _Exchange(cap, self.stores[0].tdtype, self.device)
+
+    def _enqueue_fields(self):
         self.update_fields()
         if self.validate:
+            g, stream = ctypes.byref(self._grid), self._stream()
             rho_new = self._charge_density_storage()
             _lib.call("kwb_continuity_residual", g, rho_new.data_ptr(), self._rho_prev.data_ptr(),
-                      J, E, self._G_prev.data_ptr(), self._resid.data_ptr(), stream)
+                      self._J(), self._E(), self._G_prev.data_ptr(), self._resid.data_ptr(), stream)
             self._rho_prev = rho_new
-        self.step_count += 1
+
+    def _read_status(self):
+        self._status_host.copy_(self._status, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._status_host.clone()
 
     def update_fields(self):
         """Yee leapfrog B(1/2) -> E -> B(1/2) with the current J
@@ -234,10 +282,9 @@ class Simulation:
 
     def check_status(self):
         """Read the device status words (one small D2H) and raise on any
-        contract or capacity violation; grow stores that run full."""
-        self._status_host.copy_(self._status, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
-        st = self._status_host
+        contract or capacity violation since the last step; grow stores whose
+        fullest column passed GROW_AT of its frames."""
+        st = self._read_status()
         moved = int(st[:, _lib.ST_MOVE_ERRORS].sum())
         if moved:
             raise ContractViolation(
@@ -245,11 +292,11 @@ class Simulation:
         lost = int(st[:, _lib.ST_EXCH_OVERFLOW].sum() + st[:, _lib.ST_STORE_OVERFLOW].sum())
         if lost:
             raise AllocationError(
-                f"{lost} particle(s) did not fit the exchange buffer or their super cell "
-                "this step; raise EXCHANGE_FRACTION / HEADROOM")
+                f"{lost} particle(s) did not fit their cell column or the exchange buffer "
+                "(enqueue_step has no redo; use step())")
         for i, store in enumerate(self.stores):
             store.reserve(int(st[i, _lib.ST_MAX_COUNT]))
-        return st.clone()
+        return st
 
     def run(self, steps: int):
         for _ in range(steps):

@@ -201,7 +201,7 @@ def test_store_growth_keeps_particles():
     gpu, orc = make_pair(meta, validate=False)
     st = gpu.stores[0]
     before = st.packed()
-    st.reserve(st.slots_per_sc)   # > 85% of slots -> grow
+    st.reserve(st.frames_per_sc)   # > 85% of the frames -> grow
     assert st.check_integrity()
     after = st.packed()
     for k in before:
