@@ -1,0 +1,556 @@
+// The fused particle advance: gather -> Boris push -> move -> Esirkepov
+// deposit -> in-super-cell shift, one CTA per super cell, one thread per
+// cell.  Included by particles.cu inside namespace kwb.
+//
+// Reference arithmetic: pic/kernels.py:26-135 (gather, push, move) is
+// reproduced bit for bit in float64 with no FMA contraction (the library is
+// built with --fmad=false), so particle state matches the reference exactly.
+// pic/kernels.py:153-250 (deposit) is the same density decomposition in the
+// storage precision: J is compared within tolerance, as the reference's own
+// J depends on its (thread-pool) accumulation order.
+//
+// Per-CTA shared memory:
+//   ebd   6 x (scx+2)(scy+2)(scz+2) float64  E/B + 1 guard cell, pre-widened
+//                                             (no per-particle F->D converts)
+//   jt    3 x (scx+2H)(scy+2H)(scz+2H) F      J tile incl. the shape halo
+//   queue kWarps x kWarpQ crossing records    (per warp: no block barriers)
+//   arr   V int                               in-super-cell arrivals per cell
+//   wrap  periodic index tables for staging and the J flush
+
+struct FieldPtrs {
+    const void *E[3], *B[3];
+    void *J[3];
+};
+
+constexpr int kMaxCells = 256;            // super-cell volume limit = CTA size limit
+constexpr int kWarps = kMaxCells / 32;
+constexpr int kWarpQ = 64;                // crossing-particle queue entries per warp
+
+// Yee staggers in cell units, pic/fields.py:24-31 (Ex Ey Ez Bx By Bz).
+__host__ __device__ constexpr double stagger(int c, int a) {
+    return (c == 0) ? (a == 0 ? 1.0 : 0.5)
+         : (c == 1) ? (a == 1 ? 1.0 : 0.5)
+         : (c == 2) ? (a == 2 ? 1.0 : 0.5)
+         : (c == 3) ? (a == 0 ? 0.5 : 1.0)
+         : (c == 4) ? (a == 1 ? 0.5 : 1.0)
+                    : (a == 2 ? 0.5 : 1.0);
+}
+
+struct AdvLayout {
+    int tx, ty, tz, TV, jx, jy, jz, JV;
+    size_t off_jt, off_qf, off_qi, off_arr, off_wrap, bytes;
+};
+
+template <typename F, int ORDER>
+__host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
+    constexpr int H = Shape<ORDER>::H;
+    AdvLayout L;
+    L.tx = scx + 2; L.ty = scy + 2; L.tz = scz + 2; L.TV = L.tx * L.ty * L.tz;
+    L.jx = scx + 2 * H; L.jy = scy + 2 * H; L.jz = scz + 2 * H; L.JV = L.jx * L.jy * L.jz;
+    size_t o = (size_t)6 * L.TV * sizeof(double);
+    L.off_jt = o;
+    o += (size_t)3 * L.JV * sizeof(F);
+    o = (o + 15) & ~size_t(15);
+    L.off_qf = o;
+    o += (size_t)7 * kWarps * kWarpQ * sizeof(F);
+    L.off_qi = o;
+    o += (size_t)kWarps * kWarpQ * sizeof(int);
+    L.off_arr = o;
+    o += (size_t)kMaxCells * sizeof(int);
+    L.off_wrap = o;
+    o += (size_t)(L.tx + L.ty + L.tz + L.jx + L.jy + L.jz) * sizeof(int);
+    L.bytes = (o + 15) & ~size_t(15);
+    return L;
+}
+
+// Trilinear sample of one staged (float64) component, pic/kernels.py:26-47.
+// Tile origin = super-cell origin - 1.  The floor/fraction of an axis is
+// shared by every component with the same stagger on that axis (CSE).
+template <int C>
+__device__ __forceinline__ double sample_tile(const double *__restrict__ T, double px, double py,
+                                              double pz, int ox0, int oy0, int oz0, int tx,
+                                              int txy) {
+    const double ttx = px - stagger(C, 0), tty = py - stagger(C, 1), ttz = pz - stagger(C, 2);
+    const int ix = (int)floor(ttx), iy = (int)floor(tty), iz = (int)floor(ttz);
+    const double fx = ttx - (double)ix, fy = tty - (double)iy, fz = ttz - (double)iz;
+    const double *r00 = T + (iz - oz0) * txy + (iy - oy0) * tx + (ix - ox0);
+    const double *r10 = r00 + tx;
+    const double *r01 = r00 + txy;
+    const double *r11 = r01 + tx;
+    const double gx = 1.0 - fx;
+    const double c00 = r00[0] * gx + r00[1] * fx;
+    const double c10 = r10[0] * gx + r10[1] * fx;
+    const double c01 = r01[0] * gx + r01[1] * fx;
+    const double c11 = r11[0] * gx + r11[1] * fx;
+    return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz;
+}
+
+// Shape weights at support indices 1..NS (NS = NP - 1) of a particle at
+// x in [0, 2] relative to an anchor cell: centres (i - H) + 0.5.  This is
+// the reference's _shape5_into (pic/kernels.py:138-150) for TSC, and the
+// SURVEY.md §8c CIC/PCS extension, evaluated in the compute type CT.
+template <int ORDER, typename CT>
+__device__ __forceinline__ void shape_anchor(CT x, CT (&s)[Shape<ORDER>::NP - 1]) {
+    constexpr int NP = Shape<ORDER>::NP, H = Shape<ORDER>::H;
+#pragma unroll
+    for (int i = 1; i < NP; ++i) {
+        CT d = x - (CT)((double)(i - H) + 0.5);
+        d = d < CT(0) ? -d : d;
+        CT v;
+        if (ORDER == 2) {
+            const CT e = CT(1.5) - d;
+            v = d < CT(0.5) ? CT(0.75) - d * d : (d < CT(1.5) ? CT(0.5) * e * e : CT(0));
+        } else if (ORDER == 1) {
+            v = d < CT(1) ? CT(1) - d : CT(0);
+        } else {
+            const CT e = CT(2) - d;
+            v = d < CT(1) ? (CT(4) - CT(6) * d * d + CT(3) * d * d * d) / CT(6)
+                          : (d < CT(2) ? e * e * e / CT(6) : CT(0));
+        }
+        s[i - 1] = v;
+    }
+}
+
+// Deposit of a particle that crossed a cell face (or of any particle on the
+// PCS / float64 paths) into the shared J tile, in the compute type CT
+// (float for float storage, double for double storage).  Per axis the
+// anchor is min(old cell, new cell), so old and new positions lie in [0, 2]
+// and every support fits indices 1..NS; the along-axis running sum stops at
+// NA = NP - 2 (its last entry -- the "closing" sum(s1) - sum(s0) -- is kept
+// only on axes the particle crossed; elsewhere it is a rounding residue).
+// Same density decomposition and transverse factor as pic/kernels.py:210-248
+// (factorised: T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2).  Shared
+// float atomics are CAS loops on sm_100a: this path is kept to the ~6 % of
+// particles that cross a face.
+template <typename F, int ORDER, typename CT>
+__device__ __noinline__ void deposit_cross(F *__restrict__ jt, int jx, int jy, int JV, int lx,
+                                           int ly, int lz, int dcx, int dcy, int dcz, F oox,
+                                           F ooy, F ooz, F nox, F noy, F noz, F w, double fac0,
+                                           double fac1, double fac2) {
+    constexpr int NP = Shape<ORDER>::NP, NS = NP - 1, NA = NP - 2;
+    const int dc[3] = {dcx, dcy, dcz};
+    const F oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
+    const CT fac[3] = {(CT)(fac0 * (double)w), (CT)(fac1 * (double)w), (CT)(fac2 * (double)w)};
+    CT s0[3][NS], ds[3][NS];
+    int nt[3], na[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int m = dc[a] < 0 ? -1 : 0;
+        CT s1[NS];
+        shape_anchor<ORDER, CT>((CT)oo[a] - (CT)m, s0[a]);
+        shape_anchor<ORDER, CT>((CT)no[a] + (CT)(dc[a] - m), s1);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) ds[a][i] = s1[i] - s0[a][i];
+        nt[a] = dc[a] != 0 ? NS : NS - 1;   // transverse support 1..nt
+        na[a] = dc[a] != 0 ? NA : NA - 1;   // along entries 1..na
+    }
+    const int ax = lx + min(dcx, 0), ay = ly + min(dcy, 0), az = lz + min(dcz, 0);
+    F *base = jt + (az * jy + ay) * jx + ax;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
+        CT P[NA];
+        CT run = CT(0);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) { run += ds[c][i]; P[i] = fac[c] * run; }
+        F *Jc = base + c * JV;
+#pragma unroll
+        for (int j1 = 1; j1 <= NS; ++j1) {
+            if (j1 > nt[a1]) continue;
+            const CT u = s0[a1][j1 - 1] + CT(0.5) * ds[a1][j1 - 1];
+            const CT v = CT(0.5) * s0[a1][j1 - 1] + ds[a1][j1 - 1] / CT(3);
+#pragma unroll
+            for (int j2 = 1; j2 <= NS; ++j2) {
+                if (j2 > nt[a2]) continue;
+                const CT T = u * s0[a2][j2 - 1] + v * ds[a2][j2 - 1];
+                if (T == CT(0)) continue;
+#pragma unroll
+                for (int ja = 1; ja <= NA; ++ja) {
+                    if (ja > na[c]) continue;
+                    int o;
+                    if (c == 0) o = (j2 * jy + j1) * jx + ja;
+                    else if (c == 1) o = (j1 * jy + ja) * jx + j2;
+                    else o = (ja * jy + j2) * jx + j1;
+                    const CT val = P[ja - 1] * T;
+                    if (val != CT(0)) atomicAdd(Jc + o, (F)val);
+                }
+            }
+        }
+    }
+}
+
+// Shape weights at support indices 1..3 of a particle with in-cell offset
+// x in [0, 1] (its whole CIC/TSC support), in fp32:
+//   TSC: 0.5 (1-x)^2, 0.75 - (x-1/2)^2, 0.5 x^2      (pic/kernels.py:138-150)
+//   CIC: max(1/2-x, 0), 1 - |x-1/2|, max(x-1/2, 0)
+template <int ORDER>
+__device__ __forceinline__ void shape123f(float x, float (&s)[3]) {
+    if (ORDER == 2) {
+        const float a = 1.0f - x, b = x - 0.5f;
+        s[0] = __fmul_rn(0.5f, __fmul_rn(a, a));
+        s[1] = __fmaf_rn(-b, b, 0.75f);
+        s[2] = __fmul_rn(0.5f, __fmul_rn(x, x));
+    } else {
+        s[0] = fmaxf(0.5f - x, 0.0f);
+        s[1] = 1.0f - fabsf(x - 0.5f);
+        s[2] = fmaxf(x - 0.5f, 0.0f);
+    }
+}
+
+// Register accumulation of a particle that stays in its cell (dc = 0):
+// J_a(ja, j1, j2) += P_ja * fw_a * T(j1, j2) for ja in {1, 2}, j1, j2 in
+// {1, 2, 3}, with P the running sum of ds along a and
+// T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2 (the reference's transverse
+// factor, factorised).  The closing entry ja = 3 is sum(s1) - sum(s0), a
+// rounding residue, and is dropped.  fp32 with FMA: J is compared within
+// tolerance, never bitwise (the reference's own J order is not fixed).
+struct RegAcc {
+    float a[3][2][3][3];  // [component][ja-1][j1-1][j2-1]
+};
+
+template <int ORDER>
+__device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, float ooz,
+                                             float nox, float noy, float noz, float fwx,
+                                             float fwy, float fwz) {
+    float s0[3][3], ds[3][3];
+    {
+        float s1[3];
+        shape123f<ORDER>(oox, s0[0]);
+        shape123f<ORDER>(nox, s1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ds[0][i] = __fsub_rn(s1[i], s0[0][i]);
+        shape123f<ORDER>(ooy, s0[1]);
+        shape123f<ORDER>(noy, s1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ds[1][i] = __fsub_rn(s1[i], s0[1][i]);
+        shape123f<ORDER>(ooz, s0[2]);
+        shape123f<ORDER>(noz, s1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ds[2][i] = __fsub_rn(s1[i], s0[2][i]);
+    }
+    const float fw[3] = {fwx, fwy, fwz};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;  // transverse axes: x:(y,z) y:(z,x) z:(x,y)
+        const float p1 = __fmul_rn(fw[c], ds[c][0]);
+        const float p2 = __fmul_rn(fw[c], __fadd_rn(ds[c][0], ds[c][1]));
+#pragma unroll
+        for (int j1 = 0; j1 < 3; ++j1) {
+            const float u = __fmaf_rn(0.5f, ds[a1][j1], s0[a1][j1]);
+            const float v = __fmaf_rn(1.0f / 3.0f, ds[a1][j1], __fmul_rn(0.5f, s0[a1][j1]));
+#pragma unroll
+            for (int j2 = 0; j2 < 3; ++j2) {
+                const float T = __fmaf_rn(u, s0[a2][j2], __fmul_rn(v, ds[a2][j2]));
+                R.a[c][0][j1][j2] = __fmaf_rn(p1, T, R.a[c][0][j1][j2]);
+                R.a[c][1][j1][j2] = __fmaf_rn(p2, T, R.a[c][1][j1][j2]);
+            }
+        }
+    }
+}
+
+// Tile offset of accumulator (c, ja, j1, j2) relative to the owner cell.
+__device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int jx, int jy) {
+    int ox, oy, oz;
+    if (c == 0) { ox = ja; oy = j1; oz = j2; }
+    else if (c == 1) { ox = j2; oy = ja; oz = j1; }
+    else { ox = j1; oy = j2; oz = ja; }
+    return (oz * jy + oy) * jx + ox;
+}
+
+// SX/SY/SZ: compile-time super cell (0 = runtime, from g).
+template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
+__global__ void __launch_bounds__(kMaxCells, 1)
+advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
+               int32_t *__restrict__ status) {
+    constexpr int H = Shape<ORDER>::H;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_maxcol;
+
+    const int scx = SX ? SX : g.scx, scy = SY ? SY : g.scy, scz = SZ ? SZ : g.scz;
+    const int V = scx * scy * scz;
+    const AdvLayout L = adv_layout<F, ORDER>(scx, scy, scz);
+    const int K = in.frames;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const bool owner = t < V;
+    const int sc = blockIdx.x;
+    const int bx = sc % g.gx, by = (sc / g.gx) % g.gy, bz = sc / (g.gx * g.gy);
+    const int orgx = bx * scx, orgy = by * scy, orgz = bz * scz;
+    const int lx = t % scx, ly = (t / scx) % scy, lz = t / (scx * scy);
+
+    double *ebd = reinterpret_cast<double *>(smem_raw);
+    F *jt = reinterpret_cast<F *>(smem_raw + L.off_jt);
+    F *q_f = reinterpret_cast<F *>(smem_raw + L.off_qf) + wid * kWarpQ;  // this warp's queue
+    int *q_info = reinterpret_cast<int *>(smem_raw + L.off_qi) + wid * kWarpQ;
+    constexpr int QS = kWarps * kWarpQ;                                  // column stride
+    int *arr = reinterpret_cast<int *>(smem_raw + L.off_arr);
+    int *wtx = reinterpret_cast<int *>(smem_raw + L.off_wrap);
+    int *wty = wtx + L.tx, *wtz = wty + L.ty, *wjx = wtz + L.tz, *wjy = wjx + L.jx,
+        *wjz = wjy + L.jy;
+
+    // ---- periodic index tables, then stage E/B and clear the J tile -------
+    for (int i = t; i < L.tx; i += blockDim.x) wtx[i] = pymod(orgx - 1 + i, g.nx);
+    for (int i = t; i < L.ty; i += blockDim.x) wty[i] = pymod(orgy - 1 + i, g.ny);
+    for (int i = t; i < L.tz; i += blockDim.x) wtz[i] = pymod(orgz - 1 + i, g.nz);
+    for (int i = t; i < L.jx; i += blockDim.x) wjx[i] = pymod(orgx - H + i, g.nx);
+    for (int i = t; i < L.jy; i += blockDim.x) wjy[i] = pymod(orgy - H + i, g.ny);
+    for (int i = t; i < L.jz; i += blockDim.x) wjz[i] = pymod(orgz - H + i, g.nz);
+    if (t < kMaxCells) arr[t] = 0;
+    if (t == 0) s_maxcol = 0;
+    for (int i = t; i < 3 * L.JV; i += blockDim.x) jt[i] = F(0);
+    __syncthreads();
+    {
+        const int rows = 6 * L.ty * L.tz;  // (component, z, y) rows of tx cells
+        for (int r = wid; r < rows; r += blockDim.x >> 5) {
+            const int c = r / (L.ty * L.tz), rr = r - c * (L.ty * L.tz);
+            const int d = rr / L.ty, b = rr - d * L.ty;
+            const F *src = (const F *)(c < 3 ? fp.E[c] : fp.B[c - 3]) +
+                           ((int64_t)wtz[d] * g.ny + wty[b]) * g.nx;
+            double *dst = ebd + (size_t)c * L.TV + (d * L.ty + b) * L.tx;
+            for (int a = lane; a < L.tx; a += 32) dst[a] = (double)src[wtx[a]];
+        }
+    }
+
+    const int64_t col = (int64_t)sc * V + t;
+    const int front_in = owner ? in.front[col] : 0;
+    const int back_in = owner ? in.back[col] : 0;
+    const int n_t = front_in + back_in;
+    int n_w = n_t;  // warp-uniform trip count
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n_w = max(n_w, __shfl_xor_sync(0xffffffffu, n_w, o));
+    __syncthreads();
+
+    RegAcc R;
+    if (REGACC) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) R.a[c][a][b][d] = 0.f;
+    }
+    const double qm = sp.qm_half_dt;
+    const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
+    const double cxd = (double)cx, cyd = (double)cy, czd = (double)cz;
+    const int txy = L.tx * L.ty;
+    const double *EBx = ebd, *EBy = ebd + L.TV, *EBz = ebd + 2 * L.TV, *BBx = ebd + 3 * L.TV,
+                 *BBy = ebd + 4 * L.TV, *BBz = ebd + 5 * L.TV;
+    int fo = 0;      // stayers written to the front of this column
+    int n_err = 0;
+    int wq = 0;      // this warp's queue fill (warp-uniform)
+
+    // software prefetch of the next particle's record
+    F pox = 0, poy = 0, poz = 0, pux = 0, puy = 0, puz = 0, pw = 0;
+    auto slot_of = [&](int i) -> int64_t {
+        const int k = i < front_in ? i : K - back_in + (i - front_in);
+        return ((int64_t)sc * K + k) * V + t;
+    };
+    if (0 < n_t) {
+        const int64_t q = slot_of(0);
+        pox = in.ox[q]; poy = in.oy[q]; poz = in.oz[q];
+        pux = in.ux[q]; puy = in.uy[q]; puz = in.uz[q]; pw = in.w[q];
+    }
+
+    for (int i = 0; i < n_w; ++i) {
+        const bool active = i < n_t;
+        const F ox = pox, oy = poy, oz = poz, ux = pux, uy = puy, uz = puz, w = pw;
+        if (i + 1 < n_t) {
+            const int64_t q = slot_of(i + 1);
+            pox = in.ox[q]; poy = in.oy[q]; poz = in.oz[q];
+            pux = in.ux[q]; puy = in.uy[q]; puz = in.uz[q]; pw = in.w[q];
+        }
+        bool queue = false, leave = false, mover = false, stay = false;
+        F nox = 0, noy = 0, noz = 0, nux = 0, nuy = 0, nuz = 0;
+        int dcx = 0, dcy = 0, dcz = 0, ncx = 0, ncy = 0, ncz = 0, dest = 0, nlc = 0;
+        if (active) {
+            // -- gather (pic/kernels.py:53-77): f64 compute, F store --------
+            const double px = cxd + (double)ox, py = cyd + (double)oy, pz = czd + (double)oz;
+            const int ox0 = orgx - 1, oy0 = orgy - 1, oz0 = orgz - 1;
+            const F e0 = (F)sample_tile<0>(EBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+            const F e1 = (F)sample_tile<1>(EBy, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+            const F e2 = (F)sample_tile<2>(EBz, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+            const F b0 = (F)sample_tile<3>(BBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+            const F b1 = (F)sample_tile<4>(BBy, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+            const F b2 = (F)sample_tile<5>(BBz, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+
+            // -- Boris push (pic/kernels.py:80-104), all in double ---------
+            const double qe0 = qm * (double)e0, qe1 = qm * (double)e1, qe2 = qm * (double)e2;
+            const double umx = (double)ux + qe0;
+            const double umy = (double)uy + qe1;
+            const double umz = (double)uz + qe2;
+            const double gm = sqrt(((1.0 + umx * umx) + umy * umy) + umz * umz);
+            const double ttx = (qm * (double)b0) / gm;
+            const double tty = (qm * (double)b1) / gm;
+            const double ttz = (qm * (double)b2) / gm;
+            const double tsq1 = 1.0 + ((ttx * ttx + tty * tty) + ttz * ttz);
+            const double ssx = (2.0 * ttx) / tsq1;
+            const double ssy = (2.0 * tty) / tsq1;
+            const double ssz = (2.0 * ttz) / tsq1;
+            const double upx = umx + (umy * ttz - umz * tty);
+            const double upy = umy + (umz * ttx - umx * ttz);
+            const double upz = umz + (umx * tty - umy * ttx);
+            nux = (F)((umx + (upy * ssz - upz * ssy)) + qe0);
+            nuy = (F)((umy + (upz * ssx - upx * ssz)) + qe1);
+            nuz = (F)((umz + (upx * ssy - upy * ssx)) + qe2);
+
+            // -- move (pic/kernels.py:107-135): gamma from F squares -------
+            const F sxx = nux * nux, syy = nuy * nuy, szz = nuz * nuz;
+            const double gv = sqrt(((1.0 + (double)sxx) + (double)syy) + (double)szz);
+            const double mpx = (double)ox + ((double)nux / gv) * sp.dt_d[0];
+            const double mpy = (double)oy + ((double)nuy / gv) * sp.dt_d[1];
+            const double mpz = (double)oz + ((double)nuz / gv) * sp.dt_d[2];
+            const int dxi = (int)floor(mpx), dyi = (int)floor(mpy), dzi = (int)floor(mpz);
+            nox = (F)(mpx - (double)dxi);
+            noy = (F)(mpy - (double)dyi);
+            noz = (F)(mpz - (double)dzi);
+
+            // -- cell, membership (pic/particles.py:226-228), deposit route
+            const int nlx = lx + dxi, nly = ly + dyi, nlz = lz + dzi;
+            const bool small = (unsigned)(dxi + 1) <= 2u && (unsigned)(dyi + 1) <= 2u &&
+                               (unsigned)(dzi + 1) <= 2u;
+            if (small && (unsigned)nlx < (unsigned)scx && (unsigned)nly < (unsigned)scy &&
+                (unsigned)nlz < (unsigned)scz) {
+                // still inside this super cell: no periodic wrap involved
+                dcx = dxi; dcy = dyi; dcz = dzi;
+                nlc = nlx + scx * (nly + scy * nlz);
+                if (nlc == t) stay = true; else mover = true;
+            } else {
+                ncx = pymod(cx + dxi, g.nx);
+                ncy = pymod(cy + dyi, g.ny);
+                ncz = pymod(cz + dzi, g.nz);
+                dcx = ncx - cx; dcy = ncy - cy; dcz = ncz - cz;
+                if (dcx > 1) dcx -= g.nx; else if (dcx < -1) dcx += g.nx;
+                if (dcy > 1) dcy -= g.ny; else if (dcy < -1) dcy += g.ny;
+                if (dcz > 1) dcz -= g.nz; else if (dcz < -1) dcz += g.nz;
+                dest = (ncx / scx) + g.gx * ((ncy / scy) + g.gy * (ncz / scz));
+                if (dest == sc) {
+                    nlc = (ncx - orgx) + scx * ((ncy - orgy) + scy * (ncz - orgz));
+                    if (nlc == t) stay = true; else mover = true;
+                } else {
+                    leave = true;
+                }
+            }
+            if (dcx > 1 || dcx < -1 || dcy > 1 || dcy < -1 || dcz > 1 || dcz < -1) {
+                ++n_err;  // pic/kernels.py:188-191: counted, not deposited
+            } else if (REGACC && dcx == 0 && dcy == 0 && dcz == 0) {
+                const double ww = (double)w;
+                deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox, (float)noy,
+                                    (float)noz, (float)(sp.fac[0] * ww), (float)(sp.fac[1] * ww),
+                                    (float)(sp.fac[2] * ww));
+            } else {
+                queue = true;
+            }
+        }
+
+        // ---- crossing particles -> this warp's queue (no atomics) ---------
+        const unsigned qmask = __ballot_sync(0xffffffffu, queue);
+        if (queue) {
+            const int j = wq + __popc(qmask & ((1u << lane) - 1u));
+            q_f[0 * QS + j] = ox; q_f[1 * QS + j] = oy; q_f[2 * QS + j] = oz;
+            q_f[3 * QS + j] = nox; q_f[4 * QS + j] = noy; q_f[5 * QS + j] = noz;
+            q_f[6 * QS + j] = w;
+            q_info[j] = lx | (ly << 8) | (lz << 16) | ((dcx + 1) << 24) | ((dcy + 1) << 26) |
+                        ((dcz + 1) << 28);
+        }
+        wq += __popc(qmask);
+        if (wq > kWarpQ - 32 || (i == n_w - 1 && wq > 0)) {
+            __syncwarp();
+            for (int j = lane; j < wq; j += 32) {
+                const int info = q_info[j];
+                deposit_cross<F, ORDER, F>(jt, L.jx, L.jy, L.JV, info & 255, (info >> 8) & 255,
+                                        (info >> 16) & 255, ((info >> 24) & 3) - 1,
+                                        ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
+                                        q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
+                                        q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
+                                        q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+            }
+            __syncwarp();
+            wq = 0;
+        }
+
+        // ---- write the particle to its column / the exchange --------------
+        if (stay) {
+            const int64_t o = ((int64_t)sc * K + fo) * V + t;
+            ++fo;
+            out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
+            out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
+            out.w[o] = w;
+        } else if (mover) {
+            const int slot = atomicAdd(&arr[nlc], 1);
+            if (slot < K) {
+                const int64_t o = ((int64_t)sc * K + (K - 1 - slot)) * V + nlc;
+                out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
+                out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
+                out.w[o] = w;
+            }
+        }
+        const unsigned lm = __ballot_sync(0xffffffffu, leave);
+        if (lm) {
+            int basek = 0;
+            const int leader = __ffs(lm) - 1;
+            if (lane == leader) basek = atomicAdd(ex.count, __popc(lm));
+            basek = __shfl_sync(0xffffffffu, basek, leader);
+            if (leave) {
+                const int k = basek + __popc(lm & ((1u << lane) - 1u));
+                if (k < ex.capacity) {
+                    ex.ox[k] = nox; ex.oy[k] = noy; ex.oz[k] = noz;
+                    ex.ux[k] = nux; ex.uy[k] = nuy; ex.uz[k] = nuz;
+                    ex.w[k] = w;
+                    ex.cx[k] = ncx; ex.cy[k] = ncy; ex.cz[k] = ncz;
+                    ex.dest[k] = dest;
+                } else {
+                    atomicAdd(&status[KWB_ST_EXCH_OVERFLOW], 1);
+                }
+            }
+        }
+    }
+    if (n_err) atomicAdd(&status[KWB_ST_MOVE_ERRORS], n_err);
+    __syncthreads();
+
+    // ---- reduce the register accumulators into the J tile ----------------
+    // Sweep s adds accumulator s of every cell: the targets cell + offset(s)
+    // are distinct across threads, so plain read-modify-writes are race free;
+    // the barrier orders consecutive sweeps.
+    if (REGACC) {
+        F *Jb = jt + ((lz * L.jy) + ly) * L.jx + lx;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        if (owner) {
+                            F *p = Jb + c * L.JV + regacc_offset(c, a + 1, b + 1, d + 1, L.jx, L.jy);
+                            *p = *p + (F)R.a[c][a][b][d];
+                        }
+                        __syncthreads();
+                    }
+    }
+
+    // ---- flush the J tile: coalesced red.global.add of non-zero rows ------
+    {
+        const int rows = 3 * L.jy * L.jz;
+        for (int r = wid; r < rows; r += blockDim.x >> 5) {
+            const int c = r / (L.jy * L.jz), rr = r - c * (L.jy * L.jz);
+            const int d = rr / L.jy, b = rr - d * L.jy;
+            const F *srow = jt + (size_t)c * L.JV + (d * L.jy + b) * L.jx;
+            F *drow = (F *)fp.J[c] + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
+            for (int a = lane; a < L.jx; a += 32) {
+                const F v = srow[a];
+                if (v != F(0)) atomicAdd(drow + wjx[a], v);
+            }
+        }
+    }
+    if (owner) {
+        const int nb = arr[t];
+        out.front[col] = fo;
+        out.back[col] = nb < K ? nb : K;
+        if (fo + nb > K) atomicAdd(&status[KWB_ST_STORE_OVERFLOW], fo + nb - K);
+        atomicMax(&s_maxcol, fo + nb);
+    }
+    __syncthreads();
+    if (t == 0) atomicMax(&status[KWB_ST_MAX_COUNT], s_maxcol);
+}

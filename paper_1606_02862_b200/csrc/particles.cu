@@ -19,10 +19,9 @@
 //    conflict-free barrier-separated sweeps -- no atomics at all.  Shared
 //    fp32 atomicAdd is a CAS loop on sm_100a (~2.6 ops/clk/SM measured), so
 //    this is the design's central choice.
-//  * Particles that cross a cell boundary are queued in shared memory and
-//    deposited with the reference's exact per-contribution arithmetic by
-//    all threads together (CAS into the J tile); PCS and float64 use this
-//    path for every particle.
+//  * Particles that cross a cell face are queued per warp in shared memory
+//    and deposited by the whole warp (anchor-shifted 4-point supports, CAS
+//    into the J tile); PCS and float64 use this path for every particle.
 //  * The J tile (super cell + shape halo) is flushed once with coalesced
 //    red.global.add; leavers of the super cell go to an exchange buffer.
 #include <cstdio>
@@ -31,488 +30,7 @@
 
 namespace kwb {
 
-struct FieldPtrs {
-    const void *E[3], *B[3];
-    void *J[3];
-};
-
-constexpr int kMaxCells = 256;       // super-cell volume limit (= max CTA size)
-constexpr int kQueue = 2 * kMaxCells; // crossing-particle queue capacity
-
-// Yee staggers in cell units, pic/fields.py:24-31 (Ex Ey Ez Bx By Bz).
-__host__ __device__ constexpr double stagger(int c, int a) {
-    return (c == 0) ? (a == 0 ? 1.0 : 0.5)
-         : (c == 1) ? (a == 1 ? 1.0 : 0.5)
-         : (c == 2) ? (a == 2 ? 1.0 : 0.5)
-         : (c == 3) ? (a == 0 ? 0.5 : 1.0)
-         : (c == 4) ? (a == 1 ? 0.5 : 1.0)
-                    : (a == 2 ? 0.5 : 1.0);
-}
-
-template <typename F, int ORDER>
-struct AdvanceSmem {
-    static size_t bytes(const Geo &g, int threads) {
-        constexpr int H = Shape<ORDER>::H;
-        size_t tv = (size_t)(g.scx + 2) * (g.scy + 2) * (g.scz + 2);
-        size_t jv = (size_t)(g.scx + 2 * H) * (g.scy + 2 * H) * (g.scz + 2 * H);
-        size_t b = (6 * tv + 3 * jv) * sizeof(F);
-        b = (b + 15) & ~size_t(15);
-        b += (size_t)kQueue * (7 * sizeof(F) + sizeof(int));  // crossing queue
-        b += (size_t)threads * sizeof(int);                   // intra-super-cell arrivals
-        return b;
-    }
-};
-
-// Trilinear sample of one staged component (pic/kernels.py:26-47).  The tile
-// origin is the super-cell origin minus one guard cell.
-template <typename F, int C>
-__device__ __forceinline__ double sample_tile(const F *__restrict__ T, double px, double py,
-                                              double pz, int ox0, int oy0, int oz0, int tx,
-                                              int ty) {
-    const double ttx = px - stagger(C, 0), tty = py - stagger(C, 1), ttz = pz - stagger(C, 2);
-    const double flx = floor(ttx), fly = floor(tty), flz = floor(ttz);
-    const int ix = (int)flx, iy = (int)fly, iz = (int)flz;
-    const double fx = ttx - (double)ix, fy = tty - (double)iy, fz = ttz - (double)iz;
-    const F *r00 = T + (((iz - oz0) * ty) + (iy - oy0)) * tx + (ix - ox0);
-    const F *r10 = r00 + tx;
-    const F *r01 = r00 + tx * ty;
-    const F *r11 = r01 + tx;
-    const double gx = 1.0 - fx;
-    const double c00 = (double)r00[0] * gx + (double)r00[1] * fx;
-    const double c10 = (double)r10[0] * gx + (double)r10[1] * fx;
-    const double c01 = (double)r01[0] * gx + (double)r01[1] * fx;
-    const double c11 = (double)r11[0] * gx + (double)r11[1] * fx;
-    return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz;
-}
-
-// Reference-exact deposit of one particle into the shared J tile
-// (pic/kernels.py:173-248): double transverse factor and running sum,
-// storage-type contributions.  Shared float atomics (CAS on sm_100a).
-template <typename F, int ORDER>
-__device__ void deposit_exact(F *__restrict__ jt, int jx, int jy, int JV, int lx, int ly, int lz,
-                              int dcx, int dcy, int dcz, F oox, F ooy, F ooz, F nox, F noy,
-                              F noz, F w, const double fac[3]) {
-    constexpr int NP = Shape<ORDER>::NP, TOP = NP - 2;
-    F s0x[NP], s0y[NP], s0z[NP], s1x[NP], s1y[NP], s1z[NP];
-    shape_into<F, ORDER>((double)oox, s0x);
-    shape_into<F, ORDER>((double)ooy, s0y);
-    shape_into<F, ORDER>((double)ooz, s0z);
-    shape_into<F, ORDER>((double)dcx + (double)nox, s1x);
-    shape_into<F, ORDER>((double)dcy + (double)noy, s1y);
-    shape_into<F, ORDER>((double)dcz + (double)noz, s1z);
-    const double ww = (double)w;
-    const int lox = 1 + min(dcx, 0), hix = TOP + max(dcx, 0), ex_ = min(hix, TOP);
-    const int loy = 1 + min(dcy, 0), hiy = TOP + max(dcy, 0), ey_ = min(hiy, TOP);
-    const int loz = 1 + min(dcz, 0), hiz = TOP + max(dcz, 0), ez_ = min(hiz, TOP);
-    F *J0 = jt + ((lz * jy) + ly) * jx + lx;
-    // x currents: tile[0][lx+ja][ly+j1][lz+j2]
-#pragma unroll
-    for (int j1 = 0; j1 < NP; ++j1) {
-        if (j1 < loy || j1 > hiy) continue;
-        const F dsy = s1y[j1] - s0y[j1];
-#pragma unroll
-        for (int j2 = 0; j2 < NP; ++j2) {
-            if (j2 < loz || j2 > hiz) continue;
-            const F dsz = s1z[j2] - s0z[j2];
-            const double tr = (transverse<F>(s0y[j1], dsy, s0z[j2], dsz) * fac[0]) * ww;
-            double acc = 0.0;
-#pragma unroll
-            for (int ja = 0; ja <= TOP; ++ja) {
-                if (ja < lox || ja > ex_) continue;
-                const F d = s1x[ja] - s0x[ja];
-                acc += (double)d * tr;
-                atomicAdd(J0 + (j2 * jy + j1) * jx + ja, (F)acc);
-            }
-        }
-    }
-    // y currents: tile[1][lx+j2][ly+ja][lz+j1]
-    F *J1 = J0 + JV;
-#pragma unroll
-    for (int j1 = 0; j1 < NP; ++j1) {
-        if (j1 < loz || j1 > hiz) continue;
-        const F dsz = s1z[j1] - s0z[j1];
-#pragma unroll
-        for (int j2 = 0; j2 < NP; ++j2) {
-            if (j2 < lox || j2 > hix) continue;
-            const F dsx = s1x[j2] - s0x[j2];
-            const double tr = (transverse<F>(s0z[j1], dsz, s0x[j2], dsx) * fac[1]) * ww;
-            double acc = 0.0;
-#pragma unroll
-            for (int ja = 0; ja <= TOP; ++ja) {
-                if (ja < loy || ja > ey_) continue;
-                const F d = s1y[ja] - s0y[ja];
-                acc += (double)d * tr;
-                atomicAdd(J1 + (j1 * jy + ja) * jx + j2, (F)acc);
-            }
-        }
-    }
-    // z currents: tile[2][lx+j1][ly+j2][lz+ja]
-    F *J2 = J0 + 2 * JV;
-#pragma unroll
-    for (int j1 = 0; j1 < NP; ++j1) {
-        if (j1 < lox || j1 > hix) continue;
-        const F dsx = s1x[j1] - s0x[j1];
-#pragma unroll
-        for (int j2 = 0; j2 < NP; ++j2) {
-            if (j2 < loy || j2 > hiy) continue;
-            const F dsy = s1y[j2] - s0y[j2];
-            const double tr = (transverse<F>(s0x[j1], dsx, s0y[j2], dsy) * fac[2]) * ww;
-            double acc = 0.0;
-#pragma unroll
-            for (int ja = 0; ja <= TOP; ++ja) {
-                if (ja < loz || ja > ez_) continue;
-                const F d = s1z[ja] - s0z[ja];
-                acc += (double)d * tr;
-                atomicAdd(J2 + (ja * jy + j2) * jx + j1, (F)acc);
-            }
-        }
-    }
-}
-
-// Shape values at support indices 1..3 (the whole support of a CIC/TSC
-// particle whose offset is in [0, 1]); identical arithmetic to shape_into.
-template <int ORDER>
-__device__ __forceinline__ void shape123(double x, float (&o)[3]) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        double d = x - ((double)(i + 1 - 2) + 0.5);
-        if (d < 0) d = -d;
-        double v;
-        if (ORDER == 2) {
-            if (d < 0.5) v = 0.75 - d * d;
-            else if (d < 1.5) { double e = 1.5 - d; v = (0.5 * e) * e; }
-            else v = 0.0;
-        } else {
-            v = (d < 1.0) ? 1.0 - d : 0.0;
-        }
-        o[i] = (float)v;
-    }
-}
-
-// Register accumulation of a particle that stays in its cell (dc = 0):
-// J_a(along ja, transverse j1, j2) += P_ja * fw * T(j1, j2), ja in {1, 2}
-// (the closing ja = 3 entry is a rounding residue of sum(s1) - sum(s0) and
-// is dropped), T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2.  fp32 with
-// FMA: J is compared within tolerance, never bitwise (atomic order).
-struct RegAcc {
-    float a[3][2][3][3];  // [component][ja-1][j1-1][j2-1]
-};
-
-template <int ORDER>
-__device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, float ooz,
-                                             float nox, float noy, float noz, float fwx,
-                                             float fwy, float fwz) {
-    float s0[3][3], ds[3][3];
-    {
-        float s1[3];
-        shape123<ORDER>((double)oox, s0[0]);
-        shape123<ORDER>((double)nox, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[0][i] = s1[i] - s0[0][i];
-        shape123<ORDER>((double)ooy, s0[1]);
-        shape123<ORDER>((double)noy, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[1][i] = s1[i] - s0[1][i];
-        shape123<ORDER>((double)ooz, s0[2]);
-        shape123<ORDER>((double)noz, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[2][i] = s1[i] - s0[2][i];
-    }
-    const float fw[3] = {fwx, fwy, fwz};
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;  // transverse axes (x: y,z; y: z,x; z: x,y)
-        const float p1 = ds[c][0], p2 = __fadd_rn(ds[c][0], ds[c][1]);
-#pragma unroll
-        for (int j1 = 0; j1 < 3; ++j1) {
-            const float u = __fmul_rn(fw[c], __fmaf_rn(0.5f, ds[a1][j1], s0[a1][j1]));
-            const float v = __fmul_rn(fw[c], __fmaf_rn(1.0f / 3.0f, ds[a1][j1], 0.5f * s0[a1][j1]));
-#pragma unroll
-            for (int j2 = 0; j2 < 3; ++j2) {
-                const float T = __fmaf_rn(u, s0[a2][j2], __fmul_rn(v, ds[a2][j2]));
-                R.a[c][0][j1][j2] = __fmaf_rn(p1, T, R.a[c][0][j1][j2]);
-                R.a[c][1][j1][j2] = __fmaf_rn(p2, T, R.a[c][1][j1][j2]);
-            }
-        }
-    }
-}
-
-// Tile offsets of accumulator (c, ja, j1, j2) relative to the owner cell.
-__device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int jx, int jy) {
-    int ox, oy, oz;
-    if (c == 0) { ox = ja; oy = j1; oz = j2; }
-    else if (c == 1) { ox = j2; oy = ja; oz = j1; }
-    else { ox = j1; oy = j2; oz = ja; }
-    return (oz * jy + oy) * jx + ox;
-}
-
-template <typename F, int ORDER, bool REGACC>
-__global__ void __launch_bounds__(kMaxCells)
-advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
-               int32_t *__restrict__ status) {
-    constexpr int H = Shape<ORDER>::H;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_qcount, s_nmax, s_maxcol;
-
-    const int V = g.scx * g.scy * g.scz;
-    const int K = in.frames;
-    const int t = threadIdx.x;
-    const bool owner = t < V;
-    const int sc = blockIdx.x;
-    const int bx = sc % g.gx, by = (sc / g.gx) % g.gy, bz = sc / (g.gx * g.gy);
-    const int orgx = bx * g.scx, orgy = by * g.scy, orgz = bz * g.scz;
-    const int lx = t % g.scx, ly = (t / g.scx) % g.scy, lz = t / (g.scx * g.scy);
-
-    const int tx = g.scx + 2, ty = g.scy + 2, tz = g.scz + 2, TV = tx * ty * tz;
-    const int jx = g.scx + 2 * H, jy = g.scy + 2 * H, jz = g.scz + 2 * H, JV = jx * jy * jz;
-    F *eb = reinterpret_cast<F *>(smem_raw);
-    F *jt = eb + 6 * TV;
-    size_t off = ((size_t)(6 * TV + 3 * JV) * sizeof(F) + 15) & ~size_t(15);
-    F *q_f = reinterpret_cast<F *>(smem_raw + off);           // [7][kQueue]
-    int *q_info = reinterpret_cast<int *>(q_f + 7 * kQueue);  // [kQueue]
-    int *arr = q_info + kQueue;                               // [blockDim]
-
-    // ---- stage E/B (+1 guard cell, periodic), clear J tile and counters --
-    for (int i = t; i < 6 * TV; i += blockDim.x) {
-        const int c = i / TV, r = i - c * TV;
-        const int a = r % tx, b = (r / tx) % ty, d = r / (tx * ty);
-        const int gi = pymod(orgx - 1 + a, g.nx), gj = pymod(orgy - 1 + b, g.ny),
-                  gk = pymod(orgz - 1 + d, g.nz);
-        const F *src = (const F *)(c < 3 ? fp.E[c] : fp.B[c - 3]);
-        eb[i] = src[fidx(gi, gj, gk, g.nx, g.ny)];
-    }
-    for (int i = t; i < 3 * JV; i += blockDim.x) jt[i] = F(0);
-    arr[t] = 0;
-    if (t == 0) { s_qcount = 0; s_nmax = 0; s_maxcol = 0; }
-
-    const int64_t col = (int64_t)sc * V + t;
-    const int front_in = owner ? in.front[col] : 0;
-    const int back_in = owner ? in.back[col] : 0;
-    const int n_t = front_in + back_in;
-    __syncthreads();
-    atomicMax(&s_nmax, n_t);
-    __syncthreads();
-    const int n_max = s_nmax;
-
-    RegAcc R;
-    if (REGACC) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) R.a[c][a][b][d] = 0.f;
-    }
-    const double qm = sp.qm_half_dt;
-    const int lane = t & 31;
-    const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
-    int fo = 0;      // stayers written to the front of this column
-    int n_err = 0;
-
-    for (int i = 0; i < n_max; ++i) {
-        bool active = owner && i < n_t;
-        bool queue = false, leave = false, mover = false, stay = false;
-        F ox = 0, oy = 0, oz = 0, nox = 0, noy = 0, noz = 0, nux = 0, nuy = 0, nuz = 0, w = 0;
-        int dcx = 0, dcy = 0, dcz = 0, ncx = 0, ncy = 0, ncz = 0, dest = 0, nlc = 0;
-        if (active) {
-            const int k = i < front_in ? i : K - back_in + (i - front_in);
-            const int64_t q = ((int64_t)sc * K + k) * V + t;
-            ox = in.ox[q]; oy = in.oy[q]; oz = in.oz[q];
-            const F ux = in.ux[q], uy = in.uy[q], uz = in.uz[q];
-            w = in.w[q];
-
-            // -- gather (pic/kernels.py:53-77): f64 compute, F store --------
-            const double px = (double)cx + (double)ox;
-            const double py = (double)cy + (double)oy;
-            const double pz = (double)cz + (double)oz;
-            const F e0 = (F)sample_tile<F, 0>(eb + 0 * TV, px, py, pz, orgx - 1, orgy - 1, orgz - 1, tx, ty);
-            const F e1 = (F)sample_tile<F, 1>(eb + 1 * TV, px, py, pz, orgx - 1, orgy - 1, orgz - 1, tx, ty);
-            const F e2 = (F)sample_tile<F, 2>(eb + 2 * TV, px, py, pz, orgx - 1, orgy - 1, orgz - 1, tx, ty);
-            const F b0 = (F)sample_tile<F, 3>(eb + 3 * TV, px, py, pz, orgx - 1, orgy - 1, orgz - 1, tx, ty);
-            const F b1 = (F)sample_tile<F, 4>(eb + 4 * TV, px, py, pz, orgx - 1, orgy - 1, orgz - 1, tx, ty);
-            const F b2 = (F)sample_tile<F, 5>(eb + 5 * TV, px, py, pz, orgx - 1, orgy - 1, orgz - 1, tx, ty);
-
-            // -- Boris push (pic/kernels.py:80-104), all in double ---------
-            const double umx = (double)ux + qm * (double)e0;
-            const double umy = (double)uy + qm * (double)e1;
-            const double umz = (double)uz + qm * (double)e2;
-            const double gm = sqrt(((1.0 + umx * umx) + umy * umy) + umz * umz);
-            const double ttx = (qm * (double)b0) / gm;
-            const double tty = (qm * (double)b1) / gm;
-            const double ttz = (qm * (double)b2) / gm;
-            const double tsq = (ttx * ttx + tty * tty) + ttz * ttz;
-            const double ssx = (2.0 * ttx) / (1.0 + tsq);
-            const double ssy = (2.0 * tty) / (1.0 + tsq);
-            const double ssz = (2.0 * ttz) / (1.0 + tsq);
-            const double upx = umx + (umy * ttz - umz * tty);
-            const double upy = umy + (umz * ttx - umx * ttz);
-            const double upz = umz + (umx * tty - umy * ttx);
-            nux = (F)((umx + (upy * ssz - upz * ssy)) + qm * (double)e0);
-            nuy = (F)((umy + (upz * ssx - upx * ssz)) + qm * (double)e1);
-            nuz = (F)((umz + (upx * ssy - upy * ssx)) + qm * (double)e2);
-
-            // -- move (pic/kernels.py:107-135): gamma from F squares -------
-            const F sxx = nux * nux, syy = nuy * nuy, szz = nuz * nuz;
-            const double gv = sqrt(((1.0 + (double)sxx) + (double)syy) + (double)szz);
-            const double mpx = (double)ox + ((double)nux / gv) * sp.dt_d[0];
-            const double mpy = (double)oy + ((double)nuy / gv) * sp.dt_d[1];
-            const double mpz = (double)oz + ((double)nuz / gv) * sp.dt_d[2];
-            const int dxi = (int)floor(mpx), dyi = (int)floor(mpy), dzi = (int)floor(mpz);
-            nox = (F)(mpx - (double)dxi);
-            noy = (F)(mpy - (double)dyi);
-            noz = (F)(mpz - (double)dzi);
-            ncx = pymod(cx + dxi, g.nx);
-            ncy = pymod(cy + dyi, g.ny);
-            ncz = pymod(cz + dzi, g.nz);
-
-            // -- deposit dispatch (pic/kernels.py:173-191) ------------------
-            dcx = ncx - cx; dcy = ncy - cy; dcz = ncz - cz;
-            if (dcx > 1) dcx -= g.nx; else if (dcx < -1) dcx += g.nx;
-            if (dcy > 1) dcy -= g.ny; else if (dcy < -1) dcy += g.ny;
-            if (dcz > 1) dcz -= g.nz; else if (dcz < -1) dcz += g.nz;
-            if (dcx > 1 || dcx < -1 || dcy > 1 || dcy < -1 || dcz > 1 || dcz < -1) {
-                ++n_err;
-            } else if (REGACC && dcx == 0 && dcy == 0 && dcz == 0) {
-                const double ww = (double)w;
-                deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox, (float)noy,
-                                    (float)noz, (float)(sp.fac[0] * ww), (float)(sp.fac[1] * ww),
-                                    (float)(sp.fac[2] * ww));
-            } else {
-                queue = true;
-            }
-
-            // -- membership (pic/particles.py:226-228) ----------------------
-            dest = (ncx / g.scx) + g.gx * ((ncy / g.scy) + g.gy * (ncz / g.scz));
-            if (dest == sc) {
-                nlc = (ncx - orgx) + g.scx * ((ncy - orgy) + g.scy * (ncz - orgz));
-                if (nlc == t) stay = true; else mover = true;
-            } else {
-                leave = true;
-            }
-        }
-
-        // ---- enqueue crossing particles (warp-aggregated slot claim) ------
-        {
-            const unsigned qm_ = __ballot_sync(0xffffffffu, queue);
-            if (qm_) {
-                int base = 0;
-                const int leader = __ffs(qm_) - 1;
-                if (lane == leader) base = atomicAdd(&s_qcount, __popc(qm_));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (queue) {
-                    const int j = base + __popc(qm_ & ((1u << lane) - 1u));
-                    q_f[0 * kQueue + j] = ox; q_f[1 * kQueue + j] = oy; q_f[2 * kQueue + j] = oz;
-                    q_f[3 * kQueue + j] = nox; q_f[4 * kQueue + j] = noy; q_f[5 * kQueue + j] = noz;
-                    q_f[6 * kQueue + j] = w;
-                    q_info[j] = lx | (ly << 8) | (lz << 16) | ((dcx + 1) << 24) | ((dcy + 1) << 26) |
-                                ((dcz + 1) << 28);
-                }
-            }
-        }
-        // ---- write the particle to its column / exchange ----------------
-        if (stay) {
-            const int64_t o = ((int64_t)sc * K + fo) * V + t;
-            ++fo;
-            out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
-            out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
-            out.w[o] = w;
-        } else if (mover) {
-            const int slot = atomicAdd(&arr[nlc], 1);
-            const int64_t o = ((int64_t)sc * K + (K - 1 - slot)) * V + nlc;
-            if (slot < K) {
-                out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
-                out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
-                out.w[o] = w;
-            }
-        }
-        {
-            const unsigned lm = __ballot_sync(0xffffffffu, leave);
-            if (lm) {
-                int basek = 0;
-                const int leader = __ffs(lm) - 1;
-                if (lane == leader) basek = atomicAdd(ex.count, __popc(lm));
-                basek = __shfl_sync(0xffffffffu, basek, leader);
-                if (leave) {
-                    const int k = basek + __popc(lm & ((1u << lane) - 1u));
-                    if (k < ex.capacity) {
-                        ex.ox[k] = nox; ex.oy[k] = noy; ex.oz[k] = noz;
-                        ex.ux[k] = nux; ex.uy[k] = nuy; ex.uz[k] = nuz;
-                        ex.w[k] = w;
-                        ex.cx[k] = ncx; ex.cy[k] = ncy; ex.cz[k] = ncz;
-                        ex.dest[k] = dest;
-                    } else {
-                        atomicAdd(&status[KWB_ST_EXCH_OVERFLOW], 1);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        // ---- drain the crossing queue when another round could overflow it
-        const int qn = s_qcount;
-        if (qn > kQueue - (int)blockDim.x || (i == n_max - 1 && qn > 0)) {
-            for (int j = t; j < qn; j += blockDim.x) {
-                const int info = q_info[j];
-                deposit_exact<F, ORDER>(jt, jx, jy, JV, info & 255, (info >> 8) & 255,
-                                        (info >> 16) & 255, ((info >> 24) & 3) - 1,
-                                        ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
-                                        q_f[0 * kQueue + j], q_f[1 * kQueue + j], q_f[2 * kQueue + j],
-                                        q_f[3 * kQueue + j], q_f[4 * kQueue + j], q_f[5 * kQueue + j],
-                                        q_f[6 * kQueue + j], sp.fac);
-            }
-            __syncthreads();
-            if (t == 0) s_qcount = 0;
-            __syncthreads();
-        }
-    }
-    if (n_err) atomicAdd(&status[KWB_ST_MOVE_ERRORS], n_err);
-
-    // ---- reduce the register accumulators into the J tile ----------------
-    // Sweep s adds accumulator s of every cell: targets cell + offset(s) are
-    // distinct across threads, so plain read-modify-writes are race free;
-    // the barrier orders consecutive sweeps.
-    if (REGACC) {
-        F *Jb = jt + ((lz * jy) + ly) * jx + lx;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        if (owner) {
-                            F *p = Jb + c * JV + regacc_offset(c, a + 1, b + 1, d + 1, jx, jy);
-                            *p = *p + (F)R.a[c][a][b][d];
-                        }
-                        __syncthreads();
-                    }
-    } else {
-        __syncthreads();
-    }
-
-    // ---- flush the J tile: one red.global.add per non-zero entry ---------
-    for (int i = t; i < 3 * JV; i += blockDim.x) {
-        const F v = jt[i];
-        if (v != F(0)) {
-            const int c = i / JV, r = i - c * JV;
-            const int a = r % jx, b = (r / jx) % jy, d = r / (jx * jy);
-            const int gi = pymod(orgx - H + a, g.nx), gj = pymod(orgy - H + b, g.ny),
-                      gk = pymod(orgz - H + d, g.nz);
-            atomicAdd((F *)fp.J[c] + fidx(gi, gj, gk, g.nx, g.ny), v);
-        }
-    }
-    if (owner) {
-        const int nb = arr[t];
-        out.front[col] = fo;
-        out.back[col] = nb < K ? nb : K;
-        if (fo + nb > K) atomicAdd(&status[KWB_ST_STORE_OVERFLOW], fo + nb - K);
-        atomicMax(&s_maxcol, fo + nb);
-    }
-    __syncthreads();
-    if (t == 0) atomicMax(&status[KWB_ST_MAX_COUNT], s_maxcol);
-}
+#include "advance.cuh"
 
 // Append leavers to the back of their new column (the cross-super-cell
 // shift, pic/particles.py:316-345).  Slot claims are atomic per column.
@@ -780,20 +298,21 @@ static int block_threads(const kwb_grid *g) {
     return (V + 31) / 32 * 32;
 }
 
-template <typename F, int ORDER, bool REGACC>
+template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
 static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                           void *const B[3], void *const J[3], int32_t *status,
                           cudaStream_t stream) {
     Geo geo = geo_of(*g);
     const int threads = block_threads(g);
-    size_t smem = AdvanceSmem<F, ORDER>::bytes(geo, threads);
-    auto kern = advance_kernel<F, ORDER, REGACC>;
+    const size_t smem = adv_layout<F, ORDER>(g->scx, g->scy, g->scz).bytes;
+    auto kern = advance_kernel<F, ORDER, REGACC, SX, SY, SZ>;
     if (smem > 227 * 1024) {
         kwb_set_error("super cell too large for the shared-memory tiles (%zu B)", smem);
         return KWB_EINVAL;
     }
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     FieldPtrs fp;
     for (int c = 0; c < 3; ++c) { fp.E[c] = E[c]; fp.B[c] = B[c]; fp.J[c] = J[c]; }
     if (cudaMemsetAsync(ex->count, 0, sizeof(int32_t), stream) != cudaSuccess)
@@ -802,6 +321,18 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
     kern<<<n_sc, threads, smem, stream>>>(geo, *sp, store_of<F>(*in), store_of<F>(*out),
                                           exch_of<F>(*ex), fp, status);
     return kwb_check_launch("advance_kernel");
+}
+
+// Compile-time (8,8,4) super cell (the reference default, every BASELINE
+// config) or a runtime-shaped generic instance.
+template <typename F, int ORDER, bool REGACC>
+static int dispatch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
+                            const kwb_store *out, const kwb_exchange *ex, void *const E[3],
+                            void *const B[3], void *const J[3], int32_t *status,
+                            cudaStream_t stream) {
+    if (g->scx == 8 && g->scy == 8 && g->scz == 4)
+        return launch_advance<F, ORDER, REGACC, 8, 8, 4>(g, sp, in, out, ex, E, B, J, status, stream);
+    return launch_advance<F, ORDER, REGACC, 0, 0, 0>(g, sp, in, out, ex, E, B, J, status, stream);
 }
 
 extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
@@ -823,15 +354,15 @@ extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
     cudaStream_t s = (cudaStream_t)stream;
     if (g->dtype == KWB_F32) {
         switch (shape_order) {
-            case 1: return launch_advance<float, 1, true>(g, sp, in, out, ex, E, B, J, status, s);
-            case 2: return launch_advance<float, 2, true>(g, sp, in, out, ex, E, B, J, status, s);
-            case 3: return launch_advance<float, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 1: return dispatch_advance<float, 1, true>(g, sp, in, out, ex, E, B, J, status, s);
+            case 2: return dispatch_advance<float, 2, true>(g, sp, in, out, ex, E, B, J, status, s);
+            case 3: return dispatch_advance<float, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
         }
     } else {
         switch (shape_order) {
-            case 1: return launch_advance<double, 1, false>(g, sp, in, out, ex, E, B, J, status, s);
-            case 2: return launch_advance<double, 2, false>(g, sp, in, out, ex, E, B, J, status, s);
-            case 3: return launch_advance<double, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 1: return dispatch_advance<double, 1, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 2: return dispatch_advance<double, 2, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 3: return dispatch_advance<double, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
         }
     }
     kwb_set_error("shape_order must be 1 (CIC), 2 (TSC) or 3 (PCS), got %d", shape_order);

@@ -44,7 +44,15 @@ from .pusher import MacroParticle
 FLOAT_COLUMNS = ("ox", "oy", "oz", "ux", "uy", "uz", "w")
 PACKED_FIELDS = ("cx", "cy", "cz", "ox", "oy", "oz", "ux", "uy", "uz", "w")
 HEADROOM = 1.3
-GROW_AT = 0.85
+GROW_AT = 0.75
+
+
+def initial_frames(max_col: int, mean_col: float) -> int:
+    """Frames per super cell for a fresh store: room for the fullest cell
+    plus the spread a thermal plasma develops within a few steps (cells drift
+    towards Poisson statistics; ~5 sigma over millions of cells)."""
+    return max(8, math.ceil(max_col * HEADROOM) + 4,
+               math.ceil(mean_col + 5.0 * math.sqrt(max(mean_col, 1.0))) + 6)
 
 
 class _Columns:
@@ -243,7 +251,7 @@ class SuperCellStore:
                 raise ContractViolation("particle cell index outside the grid")
             cell = (cz * ny + cy) * nx + cx
             max_col = int(torch.bincount(cell, minlength=nx * ny * nz).max().item())
-        self.frames_per_sc = max(8, math.ceil(max_col * HEADROOM) + 4)
+        self.frames_per_sc = initial_frames(max_col, n / (nx * ny * nz))
         self.loaded = n
         self._cols = [self._new_columns(), None]
         status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)

@@ -135,6 +135,8 @@ class Simulation:
         self._status = torch.zeros((len(p.species), _lib.STATUS_WORDS), dtype=torch.int32,
                                    device=self.device)
         self._status_host = torch.zeros_like(self._status, device="cpu").pin_memory()
+        self._status_ring = [torch.zeros_like(self._status_host).pin_memory() for _ in range(2)]
+        self._pending = []
         self._exchange = None
         self._rho_prev = None
         self._G_prev = None
@@ -198,13 +200,28 @@ class Simulation:
         self.check_status()
 
     def enqueue_step(self):
-        """Launch one full PIC cycle on the current stream with no host sync
-        (bench / CUDA-graph path).  Capacity and contract violations are
-        reported by the next check_status(), which raises."""
+        """Launch one full PIC cycle on the current stream without waiting for
+        it (bench path).  The status words of every step are copied to pinned
+        host memory behind an event and inspected two steps later (by then
+        the event has long completed, so no stall): columns passing GROW_AT
+        grow before they can overflow, and any violation raises at the latest
+        in check_status()."""
+        self._drain_status(keep=1)
         self._begin_step()
         self._enqueue_particles()
         self._enqueue_fields()
         self.step_count += 1
+        slot = self._status_ring[self.step_count % 2]
+        slot.copy_(self._status, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._pending.append((slot, ev))
+
+    def _drain_status(self, keep=0):
+        while len(self._pending) > keep:
+            slot, ev = self._pending.pop(0)
+            ev.synchronize()
+            self._apply_status(slot.clone())
 
     def _begin_step(self):
         if self.validate and self._rho_prev is None:
@@ -284,7 +301,12 @@ class Simulation:
         """Read the device status words (one small D2H) and raise on any
         contract or capacity violation since the last step; grow stores whose
         fullest column passed GROW_AT of its frames."""
+        self._drain_status()
         st = self._read_status()
+        self._apply_status(st)
+        return st
+
+    def _apply_status(self, st):
         moved = int(st[:, _lib.ST_MOVE_ERRORS].sum())
         if moved:
             raise ContractViolation(
@@ -296,7 +318,6 @@ class Simulation:
                 "(enqueue_step has no redo; use step())")
         for i, store in enumerate(self.stores):
             store.reserve(int(st[i, _lib.ST_MAX_COUNT]))
-        return st
 
     def run(self, steps: int):
         for _ in range(steps):
