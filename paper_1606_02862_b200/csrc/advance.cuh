@@ -179,6 +179,90 @@ __device__ __noinline__ void deposit_cross(F *__restrict__ jt, int jx, int jy, i
     }
 }
 
+// Deposit of a particle that crossed exactly one cell face, along axis k
+// (the common case: a two-axis crossing is ~40x rarer).  Axes are rotated so
+// the crossing axis is A0; with the anchor min(old, new) its supports span
+// indices 1..4, the other axes 1..3, and the footprint is exact:
+//   J_A0: along 1..3 x (A1: 1..3) x (A2: 1..3)  = 27 entries
+//   J_A1: along 1..2 x (A0: 1..4) x (A2: 1..3)  = 24 entries
+//   J_A2: along 1..2 x (A0: 1..4) x (A1: 1..3)  = 24 entries
+// (the transverse factor is symmetric in its two axes, so the reference's
+// per-component axis order does not matter).  TSC/CIC only.
+template <typename F, int ORDER>
+__device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, int JV, int k,
+                                            int lx, int ly, int lz, int dck, F oox, F ooy,
+                                            F ooz, F nox, F noy, F noz, F w, double fac0,
+                                            double fac1, double fac2) {
+    using CT = F;
+    const int a1 = k == 2 ? 0 : k + 1, a2 = k == 0 ? 2 : k - 1;
+    const F oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
+    const double fac[3] = {fac0, fac1, fac2};
+    const int st[3] = {1, jx, jx * jy};
+    const int m = dck < 0 ? -1 : 0;
+    CT s0c[4], dsc[4], s0p[3], dsp[3], s0q[3], dsq[3];
+    {
+        CT t0[Shape<ORDER>::NP - 1], t1[Shape<ORDER>::NP - 1];
+        shape_anchor<ORDER, CT>((CT)oo[k] - (CT)m, t0);
+        shape_anchor<ORDER, CT>((CT)no[k] + (CT)(dck - m), t1);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { s0c[i] = t0[i]; dsc[i] = t1[i] - t0[i]; }
+        shape_anchor<ORDER, CT>((CT)oo[a1], t0);
+        shape_anchor<ORDER, CT>((CT)no[a1], t1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) { s0p[i] = t0[i]; dsp[i] = t1[i] - t0[i]; }
+        shape_anchor<ORDER, CT>((CT)oo[a2], t0);
+        shape_anchor<ORDER, CT>((CT)no[a2], t1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) { s0q[i] = t0[i]; dsq[i] = t1[i] - t0[i]; }
+    }
+    const int lc[3] = {lx, ly, lz};
+    F *base = jt + (lc[2] + (k == 2 ? m : 0)) * st[2] + (lc[1] + (k == 1 ? m : 0)) * st[1] +
+              (lc[0] + (k == 0 ? m : 0));
+    const int sk = st[k], s1_ = st[a1], s2_ = st[a2];
+    // J_k: along k (1..3) x a1 (1..3) x a2 (1..3)
+    {
+        F *J = base + k * JV;
+        const CT fw = (CT)(fac[k] * (double)w);
+        CT P[3];
+        P[0] = fw * dsc[0];
+        P[1] = fw * (dsc[0] + dsc[1]);
+        P[2] = fw * ((dsc[0] + dsc[1]) + dsc[2]);
+#pragma unroll
+        for (int j1 = 0; j1 < 3; ++j1) {
+            const CT u = s0p[j1] + CT(0.5) * dsp[j1], v = CT(0.5) * s0p[j1] + dsp[j1] / CT(3);
+#pragma unroll
+            for (int j2 = 0; j2 < 3; ++j2) {
+                const CT T = u * s0q[j2] + v * dsq[j2];
+                F *p = J + (j1 + 1) * s1_ + (j2 + 1) * s2_;
+#pragma unroll
+                for (int ja = 0; ja < 3; ++ja) atomicAdd(p + (ja + 1) * sk, (F)(P[ja] * T));
+            }
+        }
+    }
+    // J_a1: along a1 (1..2) x k (1..4) x a2 (1..3);  J_a2: along a2 (1..2) x k x a1
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = h == 0 ? a1 : a2;
+        const CT *s0a = h == 0 ? s0p : s0q, *dsa = h == 0 ? dsp : dsq;   // along
+        const CT *s0o = h == 0 ? s0q : s0p, *dso = h == 0 ? dsq : dsp;   // the other transverse
+        const int sa = h == 0 ? s1_ : s2_, so = h == 0 ? s2_ : s1_;
+        F *J = base + c * JV;
+        const CT fw = (CT)(fac[c] * (double)w);
+        const CT P0 = fw * dsa[0], P1 = fw * (dsa[0] + dsa[1]);
+#pragma unroll
+        for (int j1 = 0; j1 < 4; ++j1) {
+            const CT u = s0c[j1] + CT(0.5) * dsc[j1], v = CT(0.5) * s0c[j1] + dsc[j1] / CT(3);
+#pragma unroll
+            for (int j2 = 0; j2 < 3; ++j2) {
+                const CT T = u * s0o[j2] + v * dso[j2];
+                F *p = J + (j1 + 1) * sk + (j2 + 1) * so;
+                atomicAdd(p + sa, (F)(P0 * T));
+                atomicAdd(p + 2 * sa, (F)(P1 * T));
+            }
+        }
+    }
+}
+
 // Shape weights at support indices 1..3 of a particle with in-cell offset
 // x in [0, 1] (its whole CIC/TSC support), in fp32:
 //   TSC: 0.5 (1-x)^2, 0.75 - (x-1/2)^2, 0.5 x^2      (pic/kernels.py:138-150)
@@ -259,7 +343,7 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
 
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
-__global__ void __launch_bounds__(kMaxCells, 1)
+__global__ void __launch_bounds__(kMaxCells, 2)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
                int32_t *__restrict__ status) {
     constexpr int H = Shape<ORDER>::H;
@@ -458,12 +542,22 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             __syncwarp();
             for (int j = lane; j < wq; j += 32) {
                 const int info = q_info[j];
-                deposit_cross<F, ORDER, F>(jt, L.jx, L.jy, L.JV, info & 255, (info >> 8) & 255,
-                                        (info >> 16) & 255, ((info >> 24) & 3) - 1,
-                                        ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
-                                        q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
-                                        q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                        q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                const int qx = info & 255, qy = (info >> 8) & 255, qz = (info >> 16) & 255;
+                const int ddx = ((info >> 24) & 3) - 1, ddy = ((info >> 26) & 3) - 1,
+                          ddz = ((info >> 28) & 3) - 1;
+                const int ncross = (ddx != 0) + (ddy != 0) + (ddz != 0);
+                if (ORDER != 3 && ncross == 1) {
+                    const int k = ddx ? 0 : (ddy ? 1 : 2);
+                    deposit_cross1<F, ORDER>(jt, L.jx, L.jy, L.JV, k, qx, qy, qz, ddx + ddy + ddz,
+                                             q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
+                                             q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
+                                             q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                } else {
+                    deposit_cross<F, ORDER, F>(jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz,
+                                               q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
+                                               q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
+                                               q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                }
             }
             __syncwarp();
             wq = 0;

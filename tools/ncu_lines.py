@@ -39,7 +39,7 @@ def sass_lines(cubin, kernel_regex):
 
 def main():
     rep, kre, cubin = sys.argv[1:4]
-    top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    top = int(sys.argv[4]) if len(sys.argv) > 4 and sys.argv[4].isdigit() else 40
     raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -64,7 +64,8 @@ def main():
         tot[0] += int(r[ie] or 0)
         tot[1] += int(r[ws] or 0)
     print(f"{fn}: {len(recs)} SASS instructions, {tot[0]:.3e} executed, {tot[1]} stall samples")
-    for line, (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+    key = 0 if "--by-inst" in sys.argv else 1
+    for line, (n, s) in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
         print(f"{line:28s} inst {100 * n / max(tot[0], 1):5.1f}%  stall {100 * s / max(tot[1], 1):5.1f}%")
 
 
