@@ -43,16 +43,18 @@ from .pusher import MacroParticle
 
 FLOAT_COLUMNS = ("ox", "oy", "oz", "ux", "uy", "uz", "w")
 PACKED_FIELDS = ("cx", "cy", "cz", "ox", "oy", "oz", "ux", "uy", "uz", "w")
-HEADROOM = 1.3
-GROW_AT = 0.75
+HEADROOM = 1.5
+GROW_AT = 0.85
 
 
 def initial_frames(max_col: int, mean_col: float) -> int:
     """Frames per super cell for a fresh store: room for the fullest cell
-    plus the spread a thermal plasma develops within a few steps (cells drift
-    towards Poisson statistics; ~5 sigma over millions of cells)."""
-    return max(8, math.ceil(max_col * HEADROOM) + 4,
-               math.ceil(mean_col + 5.0 * math.sqrt(max(mean_col, 1.0))) + 6)
+    and for the spread a thermal plasma develops (cell counts drift towards
+    Poisson statistics; the fullest of ~10^7 cells sits ~5.5 sigma above the
+    mean), with margin so that growth -- a repack plus large allocations --
+    stays out of steady-state stepping."""
+    return max(8, math.ceil(max_col * 1.3) + 4,
+               math.ceil(mean_col + 7.0 * math.sqrt(max(mean_col, 1.0))) + 8)
 
 
 class _Columns:
@@ -60,8 +62,8 @@ class _Columns:
 
     def __init__(self, n_sc, cells, frames, tdtype, device):
         n = n_sc * frames * cells
-        for c in FLOAT_COLUMNS:
-            setattr(self, c, torch.zeros(n, dtype=tdtype, device=device))
+        for c in FLOAT_COLUMNS:   # slots outside [0, front) and [K-back, K) are never read
+            setattr(self, c, torch.empty(n, dtype=tdtype, device=device))
         self.front = torch.zeros(n_sc * cells, dtype=torch.int32, device=device)
         self.back = torch.zeros(n_sc * cells, dtype=torch.int32, device=device)
         self.frames = frames
@@ -119,7 +121,7 @@ class SuperCellStore:
         if max_column <= GROW_AT * self.frames_per_sc:
             return False
         old = self.current
-        self.frames_per_sc = max(math.ceil(max_column * HEADROOM) + 4, self.frames_per_sc + 1)
+        self.frames_per_sc = max(math.ceil(max_column * HEADROOM) + 8, self.frames_per_sc + 1)
         new = self._new_columns()
         g = self._grid_struct()
         _lib.call("kwb_store_repack", _lib.ctypes.byref(g), _lib.ctypes.byref(old.cstruct()),
