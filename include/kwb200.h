@@ -155,12 +155,15 @@ int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
                    const int32_t *cx, const int32_t *cy, const int32_t *cz,
                    void *const f7[7], int32_t *status, kwb_stream_t stream);
 
-/* Export in canonical order (super cell, then local cell, then frame):
- * cell_start[n_sc * V] = exclusive scan of front + back per column.
- * Writes global cells and the 7 F arrays. */
-int kwb_store_export(const kwb_grid *g, const kwb_store *st, const int64_t *cell_start,
-                     int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
-                     kwb_stream_t stream);
+/* Export the particles of columns [col_begin, col_end) in canonical order
+ * (super cell, then local cell, then frame); cell_start[i] = output offset of
+ * column col_begin + i (exclusive scan of front + back).  Writes global
+ * cells and the 7 F arrays.  clear != 0 empties the exported columns (the
+ * z-slab decomposition extracts guard-layer leavers this way; a z-layer of
+ * super cells is a contiguous column range). */
+int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin, int64_t col_end,
+                     const int64_t *cell_start, int clear, int32_t *cx, int32_t *cy, int32_t *cz,
+                     void *const f7[7], kwb_stream_t stream);
 
 /* Copy every column into a store with a different frames_per_sc
  * (capacity growth). */

@@ -65,7 +65,7 @@ _SIGS = {
     "kwb_particle_moments": ([P, P, P, P, P], ctypes.c_int),
     "kwb_field_stats": ([P, Ptr3, Ptr3, P, P], ctypes.c_int),
     "kwb_store_load": ([P, P, I64, P, P, P, Ptr7, P, P], ctypes.c_int),
-    "kwb_store_export": ([P, P, P, P, P, P, Ptr7, P], ctypes.c_int),
+    "kwb_store_export": ([P, P, I64, I64, P, ctypes.c_int, P, P, P, Ptr7, P], ctypes.c_int),
     "kwb_store_repack": ([P, P, P, P], ctypes.c_int),
 }
 

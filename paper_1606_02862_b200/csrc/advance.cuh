@@ -371,6 +371,16 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     int *wty = wtx + L.tx, *wtz = wty + L.ty, *wjx = wtz + L.tz, *wjy = wjx + L.jx,
         *wjz = wjy + L.jy;
 
+    const int64_t col = (int64_t)sc * V + t;
+    const int front_in = owner ? in.front[col] : 0;
+    const int back_in = owner ? in.back[col] : 0;
+    const int n_t = front_in + back_in;
+    // empty super cell (e.g. a z-slab guard layer): nothing to stage or deposit
+    if (__syncthreads_or(n_t) == 0) {
+        if (owner) { out.front[col] = 0; out.back[col] = 0; }
+        return;
+    }
+
     // ---- periodic index tables, then stage E/B and clear the J tile -------
     for (int i = t; i < L.tx; i += blockDim.x) wtx[i] = pymod(orgx - 1 + i, g.nx);
     for (int i = t; i < L.ty; i += blockDim.x) wty[i] = pymod(orgy - 1 + i, g.ny);
@@ -394,10 +404,6 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         }
     }
 
-    const int64_t col = (int64_t)sc * V + t;
-    const int front_in = owner ? in.front[col] : 0;
-    const int back_in = owner ? in.back[col] : 0;
-    const int n_t = front_in + back_in;
     int n_w = n_t;  // warp-uniform trip count
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) n_w = max(n_w, __shfl_xor_sync(0xffffffffu, n_w, o));

@@ -95,19 +95,19 @@ __global__ void load_kernel(Geo g, StoreT<F> st, int64_t n, const int32_t *__res
 }
 
 template <typename F>
-__global__ void export_kernel(Geo g, StoreT<F> st, const int64_t *__restrict__ cell_start,
-                              int32_t *cx, int32_t *cy, int32_t *cz, F *ox, F *oy, F *oz, F *ux,
-                              F *uy, F *uz, F *w) {
+__global__ void export_kernel(Geo g, StoreT<F> st, int64_t col0, int64_t col1,
+                              const int64_t *__restrict__ cell_start, int clear, int32_t *cx,
+                              int32_t *cy, int32_t *cz, F *ox, F *oy, F *oz, F *ux, F *uy, F *uz,
+                              F *w) {
     const int V = g.scx * g.scy * g.scz, K = st.frames;
-    const int64_t ncol = (int64_t)g.gx * g.gy * g.gz * V;
-    for (int64_t colx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; colx < ncol;
+    for (int64_t colx = col0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; colx < col1;
          colx += (int64_t)gridDim.x * blockDim.x) {
         const int s = (int)(colx / V), c = (int)(colx % V);
         const int bx = s % g.gx, by = (s / g.gx) % g.gy, bz = s / (g.gx * g.gy);
         const int x = bx * g.scx + c % g.scx, y = by * g.scy + (c / g.scx) % g.scy,
                   z = bz * g.scz + c / (g.scx * g.scy);
         const int f = st.front[colx], b = st.back[colx];
-        int64_t o = cell_start[colx];
+        int64_t o = cell_start[colx - col0];
         for (int j = 0; j < f + b; ++j, ++o) {
             const int k = j < f ? j : K - b + (j - f);
             const int64_t q = ((int64_t)s * K + k) * V + c;
@@ -116,6 +116,7 @@ __global__ void export_kernel(Geo g, StoreT<F> st, const int64_t *__restrict__ c
             ux[o] = st.ux[q]; uy[o] = st.uy[q]; uz[o] = st.uz[q];
             w[o] = st.w[q];
         }
+        if (clear) { st.front[colx] = 0; st.back[colx] = 0; }
     }
 }
 
@@ -433,26 +434,38 @@ extern "C" int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
     return kwb_check_launch("load_kernel");
 }
 
-extern "C" int kwb_store_export(const kwb_grid *g, const kwb_store *st, const int64_t *cell_start,
+extern "C" int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin,
+                                int64_t col_end, const int64_t *cell_start, int clear,
                                 int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
                                 kwb_stream_t stream) {
     int rc = check_grid(g);
     if (rc) return rc;
     if ((rc = check_store(st, "source"))) return rc;
+    const int64_t ncol = (int64_t)g->gx * g->gy * g->gz * g->scx * g->scy * g->scz;
+    if (col_begin < 0 || col_end > ncol || col_begin > col_end) {
+        kwb_set_error("store_export: column range [%lld, %lld) outside [0, %lld)",
+                      (long long)col_begin, (long long)col_end, (long long)ncol);
+        return KWB_EINVAL;
+    }
     if (!cell_start || !cx || !cy || !cz || !f7) {
         kwb_set_error("store_export: NULL argument");
         return KWB_EINVAL;
     }
+    if (col_begin == col_end) return KWB_OK;
     Geo geo = geo_of(*g);
     cudaStream_t s = (cudaStream_t)stream;
+    const int64_t need = (col_end - col_begin + 255) / 256, cap = (int64_t)sm_count() * 16;
+    const int blocks = (int)(need < cap ? need : cap);
     if (g->dtype == KWB_F32) {
         float *const *f = (float *const *)f7;
-        export_kernel<float><<<col_blocks(g), 256, 0, s>>>(geo, store_of<float>(*st), cell_start, cx, cy, cz,
-                                                           f[0], f[1], f[2], f[3], f[4], f[5], f[6]);
+        export_kernel<float><<<blocks, 256, 0, s>>>(geo, store_of<float>(*st), col_begin, col_end,
+                                                    cell_start, clear, cx, cy, cz, f[0], f[1], f[2],
+                                                    f[3], f[4], f[5], f[6]);
     } else {
         double *const *f = (double *const *)f7;
-        export_kernel<double><<<col_blocks(g), 256, 0, s>>>(geo, store_of<double>(*st), cell_start, cx, cy, cz,
-                                                            f[0], f[1], f[2], f[3], f[4], f[5], f[6]);
+        export_kernel<double><<<blocks, 256, 0, s>>>(geo, store_of<double>(*st), col_begin, col_end,
+                                                     cell_start, clear, cx, cy, cz, f[0], f[1], f[2],
+                                                     f[3], f[4], f[5], f[6]);
     }
     return kwb_check_launch("export_kernel");
 }

@@ -1,0 +1,384 @@
+"""z-slab domain decomposition of the PIC cycle over G GPUs.
+
+The reference has no distribution; the north star asks for a
+z-decomposition over the GPUs of one box with guard-cell halos and migrating
+particles exchanged over NVLink.
+
+Layout.  Rank r owns global z-planes [r*nzl, (r+1)*nzl).  Its local grid is
+that slab plus ``gp`` guard planes on each side (gp = whole super-cell
+layers, >= 3 planes: the PCS deposit halo and the three field stages), so a
+rank runs the unmodified single-GPU kernels on an (nx, ny, nzl + 2 gp) grid.
+Particles live only in owned planes.  Per step:
+
+    advance + shift (local)        J in owned AND guard planes, movers land in
+                                   guard super cells
+    X1  J halo       guard planes of J are summed into the neighbour's owned
+                     planes (send gp planes x 3 components each way)
+    XP  particles    guard-layer columns are exported (and cleared), shipped to
+                     the neighbour, appended to its owned columns
+    Faraday 1/2 -> Ampere   (local; guard B(1/2) is computed from guard E)
+    X2  E top guard  plane <- upper neighbour's first owned plane
+    Faraday 1/2            (local)
+    X3  E/B guards   one plane each way, for the next gather / Ampere
+
+Every exchange is a set of point-to-point messages between z-neighbours
+(``DistTransport``: torch.distributed isend/irecv -- NCCL over NVLink on
+GPUs, gloo on CPU for the host-logic tests; ``LoopbackTransport``: several
+ranks driven by one process, for single-GPU verification).  With G = 1 the
+neighbour is the rank itself and the scheme reduces to periodic boundaries.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .params import SimParams
+
+E3 = ("Ex", "Ey", "Ez")
+B3 = ("Bx", "By", "Bz")
+J3 = ("Jx", "Jy", "Jz")
+
+TAG_J, TAG_PCNT, TAG_PINT, TAG_PFLT, TAG_E, TAG_EB = 0, 100, 200, 300, 400, 500
+DOWN, UP = 0, 1  # message travels to the lower / upper neighbour
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Index bookkeeping of one rank's slab (global <-> local z)."""
+
+    nx: int
+    ny: int
+    nz: int            # global
+    scz: int
+    world: int
+    rank: int
+
+    @property
+    def nzl(self) -> int:
+        return self.nz // self.world
+
+    @property
+    def ghost_layers(self) -> int:
+        return max(1, math.ceil(3 / self.scz))
+
+    @property
+    def gp(self) -> int:
+        return self.ghost_layers * self.scz
+
+    @property
+    def z0(self) -> int:
+        return self.rank * self.nzl
+
+    @property
+    def nze(self) -> int:
+        return self.nzl + 2 * self.gp
+
+    @property
+    def lower(self) -> int:
+        return (self.rank - 1) % self.world
+
+    @property
+    def upper(self) -> int:
+        return (self.rank + 1) % self.world
+
+    def validate(self):
+        if self.nz % self.world:
+            raise ValueError(f"nz={self.nz} is not divisible by {self.world} ranks")
+        if self.nzl % self.scz:
+            raise ValueError(f"slab depth {self.nzl} is not a multiple of the super cell ({self.scz})")
+        if self.nzl < self.gp:
+            raise ValueError(f"slab depth {self.nzl} is thinner than the guard region {self.gp}")
+
+    def global_z(self, zl):
+        return (np.asarray(zl) + self.z0 - self.gp) % self.nz
+
+    def owned(self) -> slice:
+        return slice(self.gp, self.gp + self.nzl)
+
+    def guard_layers(self):
+        """(bottom, top) ranges of local super-cell z-layers in the guards."""
+        g = self.ghost_layers
+        nl = self.nze // self.scz
+        return (0, g), (nl - g, nl)
+
+
+def local_params(p: SimParams, lay: SlabLayout) -> SimParams:
+    return SimParams(cells=(lay.nx, lay.ny, lay.nze), dx=p.dx, dy=p.dy, dz=p.dz, dt=p.dt,
+                     species=p.species, particles_per_cell=p.particles_per_cell,
+                     super_cell=p.super_cell, dtype=p.dtype, stream_velocity=p.stream_velocity,
+                     perturbation=p.perturbation, thermal_u=p.thermal_u, shape=p.shape)
+
+
+class LoopbackTransport:
+    """All ranks in one process: messages are delivered by copies."""
+
+    def exchange(self, sends, recvs):
+        box = {(s, d, t): x for s, d, t, x in sends}
+        for s, d, t, x in recvs:
+            x.copy_(box.pop((s, d, t)))
+        if box:
+            raise RuntimeError(f"unmatched messages {sorted(box)}")
+
+
+class DistTransport:
+    """torch.distributed point-to-point (NCCL on GPUs, gloo on CPU).  Sends
+    and receives are posted in a canonical (peer, tag) order so both sides
+    pair messages even when the lower and upper neighbour coincide (G = 2);
+    messages to self are copies."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+
+    def exchange(self, sends, recvs):
+        dist = self.dist
+        me = self.rank
+        self_box = {(s, d, t): x for s, d, t, x in sends if d == me}
+        ops = []
+        for s, d, t, x in sorted((m for m in sends if m[1] != me), key=lambda m: (m[1], m[2])):
+            ops.append(dist.P2POp(dist.isend, x.contiguous(), d, self.group, t))
+        posted = []
+        for s, d, t, x in sorted((m for m in recvs if m[0] != me), key=lambda m: (m[0], m[2])):
+            buf = x if x.is_contiguous() else torch.empty_like(x)
+            ops.append(dist.P2POp(dist.irecv, buf, s, self.group, t))
+            posted.append((buf, x))
+        for s, d, t, x in recvs:
+            if s == me:
+                x.copy_(self_box.pop((s, d, t)))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for buf, x in posted:
+            if buf is not x:
+                x.copy_(buf)
+
+
+class DecomposedSimulation:
+    """The PIC cycle on G z-slabs.  ``ranks`` are the slab indices this
+    process drives: one with DistTransport (one process per GPU), all of them
+    with LoopbackTransport."""
+
+    def __init__(self, params: SimParams, world: int, ranks, transport, backend=None,
+                 local_factory=None):
+        self.params = params
+        self.world = world
+        self.transport = transport
+        sc = params.super_cell
+        nx, ny, nz = params.cells.as_tuple()
+        self.layouts = {r: SlabLayout(nx, ny, nz, sc.z, world, r) for r in ranks}
+        for lay in self.layouts.values():
+            lay.validate()
+        if local_factory is None:
+            from .sim import Simulation
+
+            def local_factory(lp):
+                return Simulation(lp, backend=backend, validate=False)
+        self.locals = {r: local_factory(local_params(params, lay))
+                       for r, lay in self.layouts.items()}
+        self.step_count = 0
+
+    # -- state in / out --------------------------------------------------------
+    def load_global(self, fields=None, particles=None):
+        """Scatter a global state (fields: name -> (nx, ny, nz) host array;
+        particles: per species a dict of global-cell records) to the slabs."""
+        for r, lay in self.layouts.items():
+            sim = self.locals[r]
+            lf = None
+            if fields:
+                zl = lay.global_z(np.arange(lay.nze))
+                lf = {n: np.ascontiguousarray(np.asarray(a)[:, :, zl]) for n, a in fields.items()}
+            lp = None
+            if particles is not None:
+                lp = []
+                for rec in particles:
+                    cz = np.asarray(rec["cz"])
+                    m = (cz >= lay.z0) & (cz < lay.z0 + lay.nzl)
+                    d = {k: np.asarray(v)[m] for k, v in rec.items()}
+                    d["cz"] = (d["cz"] - lay.z0 + lay.gp).astype(np.int32)
+                    lp.append(d)
+            sim.load_state(fields=lf, particles=lp)
+
+    def init_khi_slabs(self, seed: int):
+        """Synthetic KHI/thermal start generated slab by slab (each rank only
+        its own super cells, stream default_rng((seed + rank, species))): the
+        multi-GPU bench path, where no rank holds the global particle set."""
+        from .sim import khi_species_particles
+        p = self.params
+        g = p.super_cell_grid
+        per_layer = g.x * g.y
+        for r, lay in self.layouts.items():
+            s0 = (lay.z0 // lay.scz) * per_layer
+            s1 = ((lay.z0 + lay.nzl) // lay.scz) * per_layer
+            parts = []
+            for i, sp in enumerate(p.species):
+                rng = np.random.default_rng((seed + r, i)) if p.thermal_u > 0 else None
+                a = khi_species_particles(p, seed + r, i, s0, s1, rng)
+                rec = {k: (v.astype(np.int32) if k in ("cx", "cy", "cz") else v.astype(p.dtype))
+                       for k, v in a.items()}
+                rec["cz"] = (rec["cz"] - lay.z0 + lay.gp).astype(np.int32)
+                rec["w"] = np.full(rec["cx"].shape, sp.weight, dtype=p.dtype)
+                parts.append(rec)
+            self.locals[r].load_state(particles=parts)
+        self.refresh_guards()
+
+    def owned_fields(self, rank, name) -> np.ndarray:
+        """Host copy of the owned planes of one lattice, (nx, ny, nzl)."""
+        lay = self.layouts[rank]
+        return self.locals[rank].fields.numpy(name)[:, :, lay.owned()]
+
+    def owned_particles(self, rank, species) -> dict:
+        """Host records of one rank's particles with GLOBAL cell indices."""
+        lay = self.layouts[rank]
+        pk = self.locals[rank].stores[species].packed()
+        pk["cz"] = lay.global_z(pk["cz"]).astype(np.int32)
+        return pk
+
+    # -- the cycle -----------------------------------------------------------------
+    def step(self):
+        for sim in self.locals.values():
+            sim._drain_status(keep=1)
+            sim.advance_particles()
+        self._exchange_j()
+        self._exchange_particles()
+        for sim in self.locals.values():
+            sim.faraday_half()
+            sim.ampere()
+        self._exchange_e_top()
+        for sim in self.locals.values():
+            sim.faraday_half()
+        self._exchange_guards()
+        for sim in self.locals.values():
+            sim.step_count += 1
+            sim._post_status()
+        self.step_count += 1
+
+    def run(self, steps):
+        for _ in range(steps):
+            self.step()
+
+    def refresh_guards(self):
+        """Make E/B guard planes consistent (after load_global)."""
+        self._exchange_guards()
+
+    def check_status(self):
+        for sim in self.locals.values():
+            sim.check_status()
+
+    def census(self) -> int:
+        n = sum(s.census() for s in self.locals.values())
+        return int(self._allreduce_sum(n))
+
+    def _allreduce_sum(self, v):
+        if isinstance(self.transport, DistTransport):
+            dev = next(iter(self.locals.values())).device
+            t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+            self.transport.dist.all_reduce(t)
+            return float(t.item())
+        return float(v)
+
+    # -- exchanges ------------------------------------------------------------
+    def _exchange_j(self):
+        sends, recvs, adds = [], [], []
+        for r, lay in self.layouts.items():
+            f = self.locals[r].fields
+            gp, nzl = lay.gp, lay.nzl
+            J = [f.storage(n) for n in J3]
+            bot = torch.stack([j[0:gp] for j in J])              # -> lower, its top owned
+            top = torch.stack([j[gp + nzl:] for j in J])         # -> upper, its bottom owned
+            sends += [(r, lay.lower, TAG_J + DOWN, bot), (r, lay.upper, TAG_J + UP, top)]
+            from_upper = torch.empty_like(bot)
+            from_lower = torch.empty_like(top)
+            recvs += [(lay.upper, r, TAG_J + DOWN, from_upper),
+                      (lay.lower, r, TAG_J + UP, from_lower)]
+            adds.append((J, nzl, gp, from_upper, from_lower))
+        self.transport.exchange(sends, recvs)
+        for J, nzl, gp, fu, fl in adds:
+            for c in range(3):
+                J[c][nzl:nzl + gp] += fu[c]
+                J[c][gp:2 * gp] += fl[c]
+
+    def _exchange_particles(self):
+        n_sp = len(self.params.species)
+        out = {}
+        cnt_sends, cnt_recvs = [], []
+        for r, lay in self.layouts.items():
+            sim = self.locals[r]
+            (b0, b1), (t0, t1) = lay.guard_layers()
+            for i, st in enumerate(sim.stores):
+                per_layer = st.sc_grid.x * st.sc_grid.y * st.capacity
+                for direction, (l0, l1), shift, peer in ((DOWN, (b0, b1), lay.nzl, lay.lower),
+                                                         (UP, (t0, t1), -lay.nzl, lay.upper)):
+                    rec = st.packed_device(columns=(l0 * per_layer, l1 * per_layer), clear=True)
+                    rec["cz"] = rec["cz"] + shift
+                    ints = torch.stack([rec["cx"], rec["cy"], rec["cz"]])
+                    flts = torch.stack([rec[c] for c in ("ox", "oy", "oz", "ux", "uy", "uz", "w")])
+                    tag = 2 * i + direction
+                    out[(r, peer, tag)] = (ints, flts)
+                    cnt_sends.append((r, peer, TAG_PCNT + tag,
+                                      torch.tensor([ints.shape[1]], dtype=torch.int64,
+                                                   device=sim.device)))
+            for i in range(n_sp):
+                for direction, peer in ((DOWN, lay.upper), (UP, lay.lower)):
+                    cnt_recvs.append((peer, r, TAG_PCNT + 2 * i + direction,
+                                      torch.zeros(1, dtype=torch.int64, device=sim.device)))
+        self.transport.exchange(cnt_sends, cnt_recvs)
+        sends, recvs, incoming = [], [], []
+        for (r, peer, tag), (ints, flts) in out.items():
+            sends += [(r, peer, TAG_PINT + tag, ints), (r, peer, TAG_PFLT + tag, flts)]
+        for src, r, tag, cnt in cnt_recvs:
+            n = int(cnt.item())
+            sim = self.locals[r]
+            i = (tag - TAG_PCNT) // 2
+            ints = torch.empty((3, n), dtype=torch.int32, device=sim.device)
+            flts = torch.empty((7, n), dtype=sim.stores[i].tdtype, device=sim.device)
+            recvs += [(src, r, TAG_PINT + tag - TAG_PCNT, ints),
+                      (src, r, TAG_PFLT + tag - TAG_PCNT, flts)]
+            incoming.append((r, i, ints, flts))
+        self.transport.exchange(sends, recvs)
+        for r, i, ints, flts in incoming:
+            if ints.shape[1] == 0:
+                continue
+            st = self.locals[r].stores[i]
+            rec = {"cx": ints[0], "cy": ints[1], "cz": ints[2]}
+            for k, c in enumerate(("ox", "oy", "oz", "ux", "uy", "uz", "w")):
+                rec[c] = flts[k]
+            st.append(rec, status=self.locals[r]._status[i])
+
+    def _exchange_e_top(self):
+        sends, recvs, sets = [], [], []
+        for r, lay in self.layouts.items():
+            f = self.locals[r].fields
+            first = torch.stack([f.storage(n)[lay.gp] for n in E3])      # -> lower's top guard
+            sends.append((r, lay.lower, TAG_E, first))
+            buf = torch.empty_like(first)
+            recvs.append((lay.upper, r, TAG_E, buf))
+            sets.append((f, lay.gp + lay.nzl, buf))
+        self.transport.exchange(sends, recvs)
+        for f, k, buf in sets:
+            for c, n in enumerate(E3):
+                f.storage(n)[k].copy_(buf[c])
+
+    def _exchange_guards(self):
+        sends, recvs, sets = [], [], []
+        for r, lay in self.layouts.items():
+            f = self.locals[r].fields
+            names = E3 + B3
+            first = torch.stack([f.storage(n)[lay.gp] for n in names])
+            last = torch.stack([f.storage(n)[lay.gp + lay.nzl - 1] for n in names])
+            sends += [(r, lay.lower, TAG_EB + DOWN, first), (r, lay.upper, TAG_EB + UP, last)]
+            from_upper = torch.empty_like(first)
+            from_lower = torch.empty_like(last)
+            recvs += [(lay.upper, r, TAG_EB + DOWN, from_upper),
+                      (lay.lower, r, TAG_EB + UP, from_lower)]
+            sets.append((f, lay, from_upper, from_lower))
+        self.transport.exchange(sends, recvs)
+        for f, lay, fu, fl in sets:
+            for c, n in enumerate(E3 + B3):
+                f.storage(n)[lay.gp + lay.nzl].copy_(fu[c])
+                f.storage(n)[lay.gp - 1].copy_(fl[c])

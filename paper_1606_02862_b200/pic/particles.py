@@ -213,21 +213,45 @@ class SuperCellStore:
         out = self.packed_device(stream)
         return {n: out[n].cpu().numpy() for n in fields}
 
-    def packed_device(self, stream=None) -> dict:
-        cnt = (self.current.front + self.current.back).to(torch.int64)
+    def packed_device(self, stream=None, columns=None, clear=False) -> dict:
+        """Export (device tensors) the particles of all columns, or of the
+        column range `columns` = (begin, end); clear=True empties them."""
+        c0, c1 = columns if columns is not None else (0, self.current.front.numel())
+        cnt = (self.current.front[c0:c1] + self.current.back[c0:c1]).to(torch.int64)
         start = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=self.device)
         torch.cumsum(cnt, 0, out=start[1:])
         n = int(start[-1].item())
         out = {c: torch.empty(n, dtype=torch.int32, device=self.device) for c in ("cx", "cy", "cz")}
         for c in FLOAT_COLUMNS:
             out[c] = torch.empty(n, dtype=self.tdtype, device=self.device)
-        if n:
+        if n or clear:
             g = self._grid_struct()
             _lib.call("kwb_store_export", _lib.ctypes.byref(g),
-                      _lib.ctypes.byref(self.current.cstruct()), start.data_ptr(),
-                      out["cx"].data_ptr(), out["cy"].data_ptr(), out["cz"].data_ptr(),
-                      _lib.ptr7([out[c] for c in FLOAT_COLUMNS]), _stream(stream, self.device))
+                      _lib.ctypes.byref(self.current.cstruct()), c0, c1, start.data_ptr(),
+                      int(bool(clear)), out["cx"].data_ptr(), out["cy"].data_ptr(),
+                      out["cz"].data_ptr(), _lib.ptr7([out[c] for c in FLOAT_COLUMNS]),
+                      _stream(stream, self.device))
         return out
+
+    def append(self, arrays: dict, stream=None, status=None) -> None:
+        """Append particle records (device tensors or host arrays; global
+        cells in this store's grid) to their columns without resizing.
+        Records that do not fit are counted in status[ST_LOAD_ERRORS] (the
+        caller's status words, checked with the step's status)."""
+        def up(a, tdt):
+            t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
+            return t.to(device=self.device, dtype=tdt, non_blocking=True).contiguous()
+        d_cells = [up(arrays[c], torch.int32) for c in ("cx", "cy", "cz")]
+        n = d_cells[0].shape[0]
+        if n == 0:
+            return
+        d_f = [up(arrays[c], self.tdtype) for c in FLOAT_COLUMNS]
+        if status is None:
+            status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)
+        g = self._grid_struct()
+        _lib.call("kwb_store_load", _lib.ctypes.byref(g), _lib.ctypes.byref(self.current.cstruct()),
+                  n, d_cells[0].data_ptr(), d_cells[1].data_ptr(), d_cells[2].data_ptr(),
+                  _lib.ptr7(d_f), status.data_ptr(), _stream(stream, self.device))
 
     def load_packed(self, arrays: dict, stream=None, presorted: bool = False) -> None:
         """Replace the store's content with particle records (global cells

@@ -211,6 +211,10 @@ class Simulation:
         self._enqueue_particles()
         self._enqueue_fields()
         self.step_count += 1
+        self._post_status()
+
+    def _post_status(self):
+        """Copy this step's status words to pinned memory behind an event."""
         slot = self._status_ring[self.step_count % 2]
         slot.copy_(self._status, non_blocking=True)
         ev = torch.cuda.Event()
@@ -275,12 +279,24 @@ class Simulation:
     def update_fields(self):
         """Yee leapfrog B(1/2) -> E -> B(1/2) with the current J
         (pic/sim.py:164-167)."""
-        p = self.params
-        g, stream = ctypes.byref(self._grid), self._stream()
-        E, B, J = self._E(), self._B(), self._J()
-        _lib.call("kwb_fields_faraday_half", g, E, B, p.dt / 2.0, stream)
-        _lib.call("kwb_fields_ampere", g, E, B, J, p.dt, stream)
-        _lib.call("kwb_fields_faraday_half", g, E, B, p.dt / 2.0, stream)
+        self.faraday_half()
+        self.ampere()
+        self.faraday_half()
+
+    def faraday_half(self):
+        """B -= dt/2 curl E (pic/kernels.py:253-269, FaradayHalfKernel)."""
+        _lib.call("kwb_fields_faraday_half", ctypes.byref(self._grid), self._E(), self._B(),
+                  self.params.dt / 2.0, self._stream())
+
+    def ampere(self):
+        """E += dt (curl B - J) (pic/kernels.py:272-288, AmpereKernel)."""
+        _lib.call("kwb_fields_ampere", ctypes.byref(self._grid), self._E(), self._B(),
+                  self._J(), self.params.dt, self._stream())
+
+    def advance_particles(self):
+        """J = 0, then every species' fused advance + shift (the particle
+        half of the cycle, pic/sim.py:138-163).  Asynchronous."""
+        self._enqueue_particles()
 
     def load_state(self, fields=None, particles=None):
         """Replace fields (name -> (nx, ny, nz) array) and/or particles (one
@@ -311,7 +327,8 @@ class Simulation:
         if moved:
             raise ContractViolation(
                 f"{moved} particle(s) moved a full cell or more before deposit")
-        lost = int(st[:, _lib.ST_EXCH_OVERFLOW].sum() + st[:, _lib.ST_STORE_OVERFLOW].sum())
+        lost = int(st[:, _lib.ST_EXCH_OVERFLOW].sum() + st[:, _lib.ST_STORE_OVERFLOW].sum()
+                   + st[:, _lib.ST_LOAD_ERRORS].sum())
         if lost:
             raise AllocationError(
                 f"{lost} particle(s) did not fit their cell column or the exchange buffer "

@@ -1,0 +1,61 @@
+"""z-slab decomposition on the CUDA path, verified on ONE GPU: G virtual
+ranks (LoopbackTransport: exchanges are copies between the ranks' buffers, so
+no kernel ever waits on another rank) against the single-domain CUDA run.
+The multi-process NCCL transport shares every line of this logic except
+DistTransport, which tests/test_decomp_cpu.py covers with gloo."""
+
+import numpy as np
+import pytest
+
+from golden_util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+FIELDS9 = ("Ex", "Ey", "Ez", "Bx", "By", "Bz", "Jx", "Jy", "Jz")
+PK = ("cx", "cy", "cz", "ox", "oy", "oz", "ux", "uy", "uz", "w")
+
+
+def _sorted(pk):
+    keys = []
+    for k in reversed(PK):
+        a = np.asarray(pk[k])
+        keys.append(a.view(np.uint64 if a.itemsize == 8 else np.uint32) if a.dtype.kind == "f" else a)
+    o = np.lexsort(keys)
+    return {k: np.asarray(pk[k])[o] for k in PK}
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("dtype,shape", [(np.float64, "tsc"), (np.float32, "tsc"), (np.float32, "pcs")])
+def test_loopback_slabs_match_single_domain(world, dtype, shape):
+    from paper_1606_02862_b200.pic import SimParams, default_species, init_khi
+    from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
+    p = SimParams(cells=(16, 16, 24), species=default_species(4, 4.0), particles_per_cell=4,
+                  dtype=np.dtype(dtype), stream_velocity=0.2, perturbation=0.05, thermal_u=0.1,
+                  shape=shape)
+    ref = init_khi(p, seed=9, validate=False)
+    dec = DecomposedSimulation(p, world, range(world), LoopbackTransport())
+    dec.load_global(particles=[st.packed() for st in ref.stores])
+    dec.refresh_guards()
+    n0 = ref.census()
+    tol = 1e-13 if np.dtype(dtype) == np.float64 else 1e-5
+    for t in range(3):
+        ref.step()
+        dec.step()
+        dec.check_status()
+        assert dec.census() == n0
+        for i in range(len(p.species)):
+            full = ref.stores[i].packed()
+            mine = _sorted({k: np.concatenate([dec.owned_particles(r, i)[k] for r in range(world)])
+                            for k in PK})
+            want = _sorted(full)
+            for k in ("cx", "cy", "cz"):
+                np.testing.assert_array_equal(mine[k], want[k], err_msg=f"step {t} {k}")
+            for k in ("ox", "oy", "oz", "ux", "uy", "uz", "w"):
+                if t == 0:
+                    np.testing.assert_array_equal(mine[k], want[k], err_msg=k)
+                else:
+                    np.testing.assert_allclose(mine[k], want[k], rtol=100 * tol, atol=1e-12)
+        for n in FIELDS9:
+            got = np.concatenate([dec.owned_fields(r, n) for r in range(world)], axis=2)
+            err = rel_l2(got, ref.fields.numpy(n))
+            assert err <= tol * (1 + 10 * t), (t, n, err)
