@@ -221,9 +221,10 @@ class SuperCellStore:
         start = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=self.device)
         torch.cumsum(cnt, 0, out=start[1:])
         n = int(start[-1].item())
-        out = {c: torch.empty(n, dtype=torch.int32, device=self.device) for c in ("cx", "cy", "cz")}
+        m = max(n, 1)  # never hand the C ABI a NULL buffer (clear with no particles)
+        out = {c: torch.empty(m, dtype=torch.int32, device=self.device) for c in ("cx", "cy", "cz")}
         for c in FLOAT_COLUMNS:
-            out[c] = torch.empty(n, dtype=self.tdtype, device=self.device)
+            out[c] = torch.empty(m, dtype=self.tdtype, device=self.device)
         if n or clear:
             g = self._grid_struct()
             _lib.call("kwb_store_export", _lib.ctypes.byref(g),
@@ -231,7 +232,7 @@ class SuperCellStore:
                       int(bool(clear)), out["cx"].data_ptr(), out["cy"].data_ptr(),
                       out["cz"].data_ptr(), _lib.ptr7([out[c] for c in FLOAT_COLUMNS]),
                       _stream(stream, self.device))
-        return out
+        return {k: v[:n] for k, v in out.items()}
 
     def append(self, arrays: dict, stream=None, status=None) -> None:
         """Append particle records (device tensors or host arrays; global

@@ -74,7 +74,7 @@ def _worker(rank, world, port, dtype, two_species, steps):
                     if t == 0:   # identical inputs -> bitwise
                         np.testing.assert_array_equal(mine[k], want[k], err_msg=f"{k}")
                     else:        # fields differ at rounding level after the halo sum
-                        np.testing.assert_allclose(mine[k], want[k], rtol=100 * tol, atol=1e-12)
+                        np.testing.assert_allclose(mine[k], want[k], rtol=100 * tol, atol=10 * tol)
             for n in FIELDS9:
                 a = dec.owned_fields(rank, n)
                 b = getattr(ref.fields, n)[:, :, lay.z0:lay.z0 + lay.nzl]
