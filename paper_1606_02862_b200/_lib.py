@@ -12,7 +12,8 @@ import os
 from .errors import NativeLibraryError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkwb200.so")
+# KWB_LIB_PATH overrides the library (A/B builds of the same ABI; never a CPU path)
+LIB_PATH = os.environ.get("KWB_LIB_PATH") or os.path.join(_HERE, "libkwb200.so")
 
 KWB_F32, KWB_F64 = 0, 1
 ST_MOVE_ERRORS, ST_EXCH_OVERFLOW, ST_STORE_OVERFLOW, ST_LEAVERS, ST_MAX_COUNT, \

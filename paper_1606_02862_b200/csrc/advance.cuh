@@ -13,7 +13,8 @@
 //   ebd   6 x (scx+2)(scy+2)(scz+2) float64  E/B + 1 guard cell, pre-widened
 //                                             (no per-particle F->D converts)
 //   jt    3 x (scx+2H)(scy+2H)(scz+2H) F      J tile incl. the shape halo
-//   queue kWarps x kWarpQ crossing records    (per warp: no block barriers)
+//   queue kWarps x kWarpQ crossing records    (per warp, deposited after the
+//                                             main loop: no block barriers)
 //   arr   V int                               in-super-cell arrivals per cell
 //   wrap  periodic index tables for staging and the J flush
 
@@ -24,7 +25,7 @@ struct FieldPtrs {
 
 constexpr int kMaxCells = 256;            // super-cell volume limit = CTA size limit
 constexpr int kWarps = kMaxCells / 32;
-constexpr int kWarpQ = 64;                // crossing-particle queue entries per warp
+constexpr int kWarpQ = 160;               // crossing-particle queue entries per warp
 
 // Yee staggers in cell units, pic/fields.py:24-31 (Ex Ey Ez Bx By Bz).
 __host__ __device__ constexpr double stagger(int c, int a) {
@@ -343,7 +344,10 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
 
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
-__global__ void __launch_bounds__(kMaxCells, 2)
+#ifndef KWB_MIN_BLOCKS
+#define KWB_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(kMaxCells, KWB_MIN_BLOCKS)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
                int32_t *__restrict__ status) {
     constexpr int H = Shape<ORDER>::H;
@@ -442,6 +446,32 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         pux = in.ux[q]; puy = in.uy[q]; puz = in.uz[q]; pw = in.w[q];
     }
 
+    // Deposit the queued crossing particles of this warp (lanes take one
+    // record each; CAS into the J tile).
+    auto drain_queue = [&]() {
+            __syncwarp();
+            for (int j = lane; j < wq; j += 32) {
+                const int info = q_info[j];
+                const int qx = info & 255, qy = (info >> 8) & 255, qz = (info >> 16) & 255;
+                const int ddx = ((info >> 24) & 3) - 1, ddy = ((info >> 26) & 3) - 1,
+                          ddz = ((info >> 28) & 3) - 1;
+                const int ncross = (ddx != 0) + (ddy != 0) + (ddz != 0);
+                if (ORDER != 3 && ncross == 1) {
+                    const int k = ddx ? 0 : (ddy ? 1 : 2);
+                    deposit_cross1<F, ORDER>(jt, L.jx, L.jy, L.JV, k, qx, qy, qz, ddx + ddy + ddz,
+                                             q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
+                                             q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
+                                             q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                } else {
+                    deposit_cross<F, ORDER, F>(jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz,
+                                               q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
+                                               q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
+                                               q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                }
+            }
+            __syncwarp();
+            };
+
     for (int i = 0; i < n_w; ++i) {
         const bool active = i < n_t;
         const F ox = pox, oy = poy, oz = poz, ux = pux, uy = puy, uz = puz, w = pw;
@@ -457,12 +487,17 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             // -- gather (pic/kernels.py:53-77): f64 compute, F store --------
             const double px = cxd + (double)ox, py = cyd + (double)oy, pz = czd + (double)oz;
             const int ox0 = orgx - 1, oy0 = orgy - 1, oz0 = orgz - 1;
+#ifndef KWB_EXP_NOGATHER
             const F e0 = (F)sample_tile<0>(EBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F e1 = (F)sample_tile<1>(EBy, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F e2 = (F)sample_tile<2>(EBz, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F b0 = (F)sample_tile<3>(BBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F b1 = (F)sample_tile<4>(BBy, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F b2 = (F)sample_tile<5>(BBz, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+#else   // timing experiment only: no field gather
+            const F e0 = (F)(px * 1e-30), e1 = (F)(py * 1e-30), e2 = (F)(pz * 1e-30);
+            const F b0 = e0, b1 = e1, b2 = e2;
+#endif
 
             // -- Boris push (pic/kernels.py:80-104), all in double ---------
             const double qe0 = qm * (double)e0, qe1 = qm * (double)e1, qe2 = qm * (double)e2;
@@ -523,13 +558,19 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             }
             if (dcx > 1 || dcx < -1 || dcy > 1 || dcy < -1 || dcz > 1 || dcz < -1) {
                 ++n_err;  // pic/kernels.py:188-191: counted, not deposited
-            } else if (REGACC && dcx == 0 && dcy == 0 && dcz == 0) {
+            }
+#ifdef KWB_EXP_NODEPOSIT   // timing experiment only: no current deposit
+            else if (true) { }
+#endif
+            else if (REGACC && dcx == 0 && dcy == 0 && dcz == 0) {
                 const double ww = (double)w;
                 deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox, (float)noy,
                                     (float)noz, (float)(sp.fac[0] * ww), (float)(sp.fac[1] * ww),
                                     (float)(sp.fac[2] * ww));
             } else {
+#ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
                 queue = true;
+#endif
             }
         }
 
@@ -544,28 +585,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                         ((dcz + 1) << 28);
         }
         wq += __popc(qmask);
-        if (wq > kWarpQ - 32 || (i == n_w - 1 && wq > 0)) {
-            __syncwarp();
-            for (int j = lane; j < wq; j += 32) {
-                const int info = q_info[j];
-                const int qx = info & 255, qy = (info >> 8) & 255, qz = (info >> 16) & 255;
-                const int ddx = ((info >> 24) & 3) - 1, ddy = ((info >> 26) & 3) - 1,
-                          ddz = ((info >> 28) & 3) - 1;
-                const int ncross = (ddx != 0) + (ddy != 0) + (ddz != 0);
-                if (ORDER != 3 && ncross == 1) {
-                    const int k = ddx ? 0 : (ddy ? 1 : 2);
-                    deposit_cross1<F, ORDER>(jt, L.jx, L.jy, L.JV, k, qx, qy, qz, ddx + ddy + ddz,
-                                             q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
-                                             q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                             q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
-                } else {
-                    deposit_cross<F, ORDER, F>(jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz,
-                                               q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
-                                               q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                               q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
-                }
-            }
-            __syncwarp();
+        if (wq > kWarpQ - 32) {   // rare: the queue is normally drained after the loop
+            drain_queue();
             wq = 0;
         }
 
@@ -629,6 +650,12 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                         __syncthreads();
                     }
     }
+
+    // ---- deposit the crossing particles queued during the loop -----------
+    // (after the accumulator sweeps, when nothing else is live, so the
+    // out-of-line deposit routines run without spilling the accumulators)
+    if (wq > 0) drain_queue();
+    __syncthreads();
 
     // ---- flush the J tile: coalesced red.global.add of non-zero rows ------
     {
