@@ -16,6 +16,7 @@
  *   kwb_continuity_residual<- the validate block  pic/sim.py:168-175
  *   kwb_particle_moments / kwb_field_stats
  *                          <- Simulation.diagnostics pic/sim.py:191-225
+ *   kwb_init_khi           <- init_khi (on-device path)  pic/sim.py:239-302
  *   kwb_store_load / kwb_store_export
  *                          <- _bulk_fill / SuperCellStore.packed
  *                             pic/sim.py:305-328, pic/particles.py:174-186
@@ -104,6 +105,18 @@ typedef struct kwb_exchange {
     int32_t capacity;
 } kwb_exchange;
 
+typedef struct kwb_init {
+    int32_t ppc, px, py, pz;       /* quiet-start sub-lattice, ppc = px*py*pz (pic/sim.py:36-52) */
+    double stream_velocity;        /* KHI v0 (pic/params.py:48) */
+    double perturbation;           /* KHI v_y amplitude (pic/params.py:49) */
+    double thermal_u;              /* N(0, thermal_u^2) per momentum component */
+    double weight;                 /* macro-particle weight of the species */
+    uint64_t seed;                 /* Philox key (with the species index) */
+    int32_t species_index;
+    int32_t x_offset, y_offset, z_offset; /* global cell of local cell 0 (z-slabs) */
+    int32_t global_nx, global_ny;  /* global extents for the KHI profile */
+} kwb_init;
+
 int kwb_version(void);
 const char *kwb_last_error(void);
 
@@ -164,6 +177,12 @@ int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
 int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin, int64_t col_end,
                      const int64_t *cell_start, int clear, int32_t *cx, int32_t *cy, int32_t *cz,
                      void *const f7[7], kwb_stream_t stream);
+
+/* On-device KHI/thermal start (pic/sim.py:239-302 semantics, Philox jitter):
+ * fills every cell column with the ppc quiet-start particles of the species.
+ * The store's front/back are set; frames_per_sc must be >= ppc. */
+int kwb_init_khi(const kwb_grid *g, const kwb_init *ini, const kwb_store *st,
+                 kwb_stream_t stream);
 
 /* Copy every column into a store with a different frames_per_sc
  * (capacity growth). */

@@ -50,6 +50,14 @@ class ExchangeC(ctypes.Structure):
                 ("capacity", I32)]
 
 
+class InitC(ctypes.Structure):
+    _fields_ = [("ppc", I32), ("px", I32), ("py", I32), ("pz", I32),
+                ("stream_velocity", D), ("perturbation", D), ("thermal_u", D), ("weight", D),
+                ("seed", ctypes.c_uint64), ("species_index", I32),
+                ("x_offset", I32), ("y_offset", I32), ("z_offset", I32),
+                ("global_nx", I32), ("global_ny", I32)]
+
+
 Ptr3 = P * 3
 Ptr7 = P * 7
 
@@ -68,6 +76,7 @@ _SIGS = {
     "kwb_store_load": ([P, P, I64, P, P, P, Ptr7, P, P], ctypes.c_int),
     "kwb_store_export": ([P, P, I64, I64, P, ctypes.c_int, P, P, P, Ptr7, P], ctypes.c_int),
     "kwb_store_repack": ([P, P, P, P], ctypes.c_int),
+    "kwb_init_khi": ([P, P, P, P], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -204,12 +204,28 @@ class DecomposedSimulation:
                     lp.append(d)
             sim.load_state(fields=lf, particles=lp)
 
-    def init_khi_slabs(self, seed: int):
-        """Synthetic KHI/thermal start generated slab by slab (each rank only
-        its own super cells, stream default_rng((seed + rank, species))): the
-        multi-GPU bench path, where no rank holds the global particle set."""
+    def init_khi_slabs(self, seed: int, rng: str = "device"):
+        """KHI/thermal start generated slab by slab -- no rank holds the
+        global particle set.  rng="device": kwb_init_khi with global cell
+        offsets (the result does not depend on the number of slabs);
+        rng="numpy": host generation of the slab's super cells with the
+        stream default_rng((seed + rank, species))."""
         from .sim import khi_species_particles
         p = self.params
+        if rng == "device":
+            for r, lay in self.layouts.items():
+                sim = self.locals[r]
+                for i, st in enumerate(sim.stores):
+                    st.init_device(p, i, seed, offsets=(0, 0, lay.z0 - lay.gp),
+                                   global_cells=p.cells.as_tuple())
+                    # guard layers start empty: clear their columns
+                    per_layer = st.sc_grid.x * st.sc_grid.y * st.capacity
+                    (b0, b1), (t0, t1) = lay.guard_layers()
+                    for l0, l1 in ((b0, b1), (t0, t1)):
+                        st.current.front[l0 * per_layer:l1 * per_layer] = 0
+                    st.loaded = st.census()
+            self.refresh_guards()
+            return
         g = p.super_cell_grid
         per_layer = g.x * g.y
         for r, lay in self.layouts.items():

@@ -290,6 +290,31 @@ class SuperCellStore:
         if bad:
             raise AllocationError(f"{bad} particle record(s) could not be loaded")
 
+    def init_device(self, params, species_index: int, seed: int, offsets=(0, 0, 0),
+                    global_cells=None, stream=None) -> None:
+        """Fill the store with init_khi's quiet-start particles on the device
+        (kwb_init_khi): same placement and velocity profile as the host path,
+        thermal jitter from Philox instead of numpy's default_rng."""
+        from .sim import _near_cubic_factors
+        ppc = params.particles_per_cell
+        px, py, pz = _near_cubic_factors(ppc)
+        n_cells = self.cells.volume
+        self.frames_per_sc = initial_frames(ppc, float(ppc))
+        self._cols = [self._new_columns(), None]
+        gx, gy = (global_cells or self.cells.as_tuple())[:2]
+        ini = _lib.InitC(ppc=ppc, px=px, py=py, pz=pz,
+                         stream_velocity=params.stream_velocity,
+                         perturbation=params.perturbation, thermal_u=params.thermal_u,
+                         weight=params.species[species_index].weight,
+                         seed=int(seed) & 0xFFFFFFFFFFFFFFFF, species_index=species_index,
+                         x_offset=offsets[0], y_offset=offsets[1], z_offset=offsets[2],
+                         global_nx=gx, global_ny=gy)
+        g = self._grid_struct()
+        g.dx, g.dy, g.dz = params.dx, params.dy, params.dz
+        _lib.call("kwb_init_khi", _lib.ctypes.byref(g), _lib.ctypes.byref(ini),
+                  _lib.ctypes.byref(self.current.cstruct()), _stream(stream, self.device))
+        self.loaded = n_cells * ppc
+
     def insert(self, p: MacroParticle) -> None:
         """Append one particle to its cell column (host-side path,
         pic/particles.py:129-144)."""

@@ -472,14 +472,24 @@ def khi_species_particles(params: SimParams, seed: int, sp_i: int, sc_begin: int
 
 
 def init_khi(params: SimParams, seed: int = 0, backend=None, strategy="elements",
-             validate=True, chunk_super_cells: int = 4096) -> Simulation:
+             validate=True, chunk_super_cells: int = 4096, rng: str = "numpy") -> Simulation:
     """Kelvin-Helmholtz setup (pic/sim.py:239-302): counter-streaming layers
     split along y, sinusoidal v_y perturbation, quiet-start placement,
-    thermal jitter from default_rng((seed, species_index)); E = B = 0.
-    Generated on the host in the reference's exact draw order (bitwise the
-    same initial state), then uploaded into the device stores."""
+    thermal jitter; E = B = 0.
+
+    rng="numpy" (default): generated on the host in the reference's exact
+    default_rng((seed, species_index)) draw order -- bitwise the reference's
+    initial state -- then uploaded.  rng="device": generated in HBM by
+    kwb_init_khi (same placement/profile, Philox jitter), for 10^8-10^9
+    particles where the host path takes minutes."""
     sim = Simulation(params, backend=backend, strategy=strategy, validate=validate)
     p = params
+    if rng == "device":
+        for sp_i, store in enumerate(sim.stores):
+            store.init_device(p, sp_i, seed)
+        return sim
+    if rng != "numpy":
+        raise ValueError(f"rng must be 'numpy' or 'device', got {rng!r}")
     n_sc = p.super_cell_grid.volume
     dt = p.dtype
     for sp_i, (species, store) in enumerate(zip(p.species, sim.stores)):
