@@ -1,0 +1,151 @@
+"""Edge cases of the CUDA path against the oracle (bitwise particle state after
+one step from identical state, fields within tolerance):
+
+* empty store, a single particle, one particle per cell;
+* offsets exactly 0 and exactly 1.0 (the f32 rounding case the reference
+  keeps), particles on super-cell faces;
+* near-light-speed momenta (the largest per-step displacement CFL allows);
+* a grid that is a single super cell along an axis (periodic self-wrap, the
+  super-cell shift returns the particle to the same super cell);
+* non-default super cells ((4,4,4): 64 threads per CTA), anisotropic cells;
+* PCS and CIC in float64.
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import rel_l2
+from parity_util import FIELDS9, assert_particles_bitwise
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(cells, species, dtype, shape="tsc", super_cell=(8, 8, 4), deltas=(1.0, 1.0, 1.0)):
+    from oracle.pic import OracleSim
+    from paper_1606_02862_b200.pic import SimParams, Simulation
+    p = SimParams(cells=cells, species=species, dtype=dtype, shape=shape, super_cell=super_cell,
+                  dx=deltas[0], dy=deltas[1], dz=deltas[2])
+    gpu = Simulation(p, validate=True)
+    orc = OracleSim(p, validate=True, shape_order=p.shape_order, threads=2)
+    return p, gpu, orc
+
+
+def _load(p, gpu, orc, records):
+    """records: list (per species) of dicts of global-cell particle arrays."""
+    gpu.load_state(particles=records)
+    for st, rec in zip(orc.stores, records):
+        scx, scy, scz = st.super_cell
+        gx, gy, _ = st.sc_grid
+        cx, cy, cz = (np.asarray(rec[k]).astype(np.int64) for k in ("cx", "cy", "cz"))
+        sc = cx // scx + gx * (cy // scy + gy * (cz // scz))
+        o = np.argsort(sc, kind="stable")
+        st.load_packed(sc[o], {k: np.asarray(v)[o] for k, v in rec.items()})
+
+
+def _step_and_compare(p, gpu, orc, steps=2, tol=None):
+    dt = np.dtype(p.dtype)
+    tol = tol or (1e-12 if dt == np.float64 else 1e-5)
+    for t in range(steps):
+        if t:
+            gpu.load_state(fields={n: getattr(orc.fields, n) for n in FIELDS9},
+                           particles=[st.packed() for st in orc.stores])
+        gpu.step()
+        orc.step()
+        for gs, os_ in zip(gpu.stores, orc.stores):
+            assert_particles_bitwise(gs, os_)
+        for n in FIELDS9:
+            err = rel_l2(gpu.fields.numpy(n), getattr(orc.fields, n))
+            assert err <= tol, (t, n, err)
+        assert gpu.last_residual <= (1e-12 if dt == np.float64 else 1e-6)
+
+
+def _rec(cells_xyz, offs, us, w, dtype):
+    c = np.asarray(cells_xyz, dtype=np.int32)
+    o = np.asarray(offs, dtype=dtype)
+    u = np.asarray(us, dtype=dtype)
+    return dict(cx=c[:, 0], cy=c[:, 1], cz=c[:, 2], ox=o[:, 0], oy=o[:, 1], oz=o[:, 2],
+                ux=u[:, 0], uy=u[:, 1], uz=u[:, 2], w=np.full(len(c), w, dtype=dtype))
+
+
+def _electron(w=1.0):
+    from paper_1606_02862_b200.pic import Species
+    return (Species("electron", -1.0, 1.0, w),)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_empty_store_steps(dtype):
+    p, gpu, orc = _pair((16, 16, 8), _electron(), dtype)
+    gpu.step()
+    assert gpu.census() == 0
+    for n in FIELDS9:
+        assert float(np.abs(gpu.fields.numpy(n)).max()) == 0.0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_single_fast_particle_crossing_faces(dtype):
+    """One electron at u ~ 7 c moving diagonally across super-cell faces and
+    the periodic boundary (largest CFL displacement)."""
+    p, gpu, orc = _pair((16, 16, 8), _electron(0.5), dtype)
+    rec = _rec([[15, 7, 7]], [[0.9, 0.99, 0.95]], [[4.0, 4.0, 4.0]], 0.5, dtype)
+    _load(p, gpu, orc, [rec])
+    _step_and_compare(p, gpu, orc, steps=3)
+
+
+def test_offsets_exactly_zero_and_one_f32():
+    """fp32 offsets of exactly 0.0 and 1.0 (1.0 arises from rounding in the
+    reference's move and must be carried, not clamped)."""
+    dtype = np.float32
+    p, gpu, orc = _pair((16, 16, 8), _electron(0.25), dtype)
+    cells, offs, us = [], [], []
+    rng = np.random.default_rng(1)
+    for i in range(64):
+        cells.append([rng.integers(0, 16), rng.integers(0, 16), rng.integers(0, 8)])
+        o = rng.choice([0.0, 1.0, np.float32(1.0) - np.float32(2.0 ** -24), 0.5], size=3)
+        offs.append(o)
+        us.append(rng.normal(0.0, 0.3, 3))
+    _load(p, gpu, orc, [_rec(cells, offs, us, 0.25, dtype)])
+    _step_and_compare(p, gpu, orc, steps=2)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_single_super_cell_per_axis_selfwrap(dtype):
+    """cells == super cell along x and z: leaving through a face re-enters
+    the same super cell (periodic self-wrap)."""
+    from paper_1606_02862_b200.pic import default_species
+    p, gpu, orc = _pair((8, 16, 4), default_species(2, 1.0), dtype)
+    rng = np.random.default_rng(2)
+    n = 300
+    recs = []
+    for s in range(2):
+        c = np.stack([rng.integers(0, 8, n), rng.integers(0, 16, n), rng.integers(0, 4, n)], 1)
+        recs.append(_rec(c, rng.random((n, 3)), rng.normal(0.0, 1.0, (n, 3)), 0.5, dtype))
+    _load(p, gpu, orc, recs)
+    _step_and_compare(p, gpu, orc, steps=3)
+
+
+@pytest.mark.parametrize("shape", ["cic", "tsc", "pcs"])
+def test_small_super_cell_anisotropic_f64(shape):
+    """(4,4,4) super cells (64-thread CTAs, generic kernel instance),
+    anisotropic cell sizes, every shape in float64."""
+    from paper_1606_02862_b200.pic import default_species
+    p, gpu, orc = _pair((8, 12, 8), default_species(2, 3.0), np.float64, shape=shape,
+                        super_cell=(4, 4, 4), deltas=(0.7, 1.0, 1.3))
+    rng = np.random.default_rng(3)
+    n = 400
+    recs = []
+    for s in range(2):
+        c = np.stack([rng.integers(0, 8, n), rng.integers(0, 12, n), rng.integers(0, 8, n)], 1)
+        recs.append(_rec(c, rng.random((n, 3)), rng.normal(0.0, 0.5, (n, 3)), 0.5, np.float64))
+    _load(p, gpu, orc, recs)
+    _step_and_compare(p, gpu, orc, steps=3)
+
+
+def test_one_particle_per_cell_dense_columns():
+    from paper_1606_02862_b200.pic import SimParams, Species, init_khi
+    from oracle.pic import oracle_init_khi
+    p = SimParams(cells=(16, 16, 16), species=(Species("e", -1.0, 1.0, 1.0),),
+                  particles_per_cell=1, dtype=np.float32, stream_velocity=0.0,
+                  perturbation=0.0, thermal_u=0.2)
+    gpu = init_khi(p, seed=8, validate=True)
+    orc = oracle_init_khi(p, seed=8, validate=True, threads=2)
+    _step_and_compare(p, gpu, orc, steps=2)
