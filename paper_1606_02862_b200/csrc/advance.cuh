@@ -396,6 +396,34 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     if (t == 0) s_maxcol = 0;
     for (int i = t; i < 3 * L.JV; i += blockDim.x) jt[i] = F(0);
     __syncthreads();
+#ifndef KWB_EXP_ROWSTAGE
+    {
+        // flat over (component, z, y, x) so every lane works, and batches of
+        // kStageB independent loads in flight per thread (one memory latency
+        // per batch instead of one per tile row)
+        constexpr int kStageB = 8;
+        const int total = 6 * L.TV, nth = blockDim.x, txy_ = L.tx * L.ty;
+        for (int base = t; base < total; base += kStageB * nth) {
+            F v[kStageB];
+#pragma unroll
+            for (int u = 0; u < kStageB; ++u) {
+                const int i = base + u * nth;
+                if (i < total) {
+                    const int c = i / L.TV, r = i - c * L.TV;
+                    const int d = r / txy_, r2 = r - d * txy_;
+                    const int b = r2 / L.tx, a = r2 - b * L.tx;
+                    const F *src = (const F *)(c < 3 ? fp.E[c] : fp.B[c - 3]);
+                    v[u] = __ldg(src + ((int64_t)wtz[d] * g.ny + wty[b]) * g.nx + wtx[a]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kStageB; ++u) {
+                const int i = base + u * nth;
+                if (i < total) ebd[i] = (double)v[u];
+            }
+        }
+    }
+#else
     {
         const int rows = 6 * L.ty * L.tz;  // (component, z, y) rows of tx cells
         for (int r = wid; r < rows; r += blockDim.x >> 5) {
@@ -407,6 +435,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             for (int a = lane; a < L.tx; a += 32) dst[a] = (double)src[wtx[a]];
         }
     }
+#endif
 
     int n_w = n_t;  // warp-uniform trip count
 #pragma unroll
@@ -659,15 +688,14 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
     // ---- flush the J tile: coalesced red.global.add of non-zero rows ------
     {
-        const int rows = 3 * L.jy * L.jz;
-        for (int r = wid; r < rows; r += blockDim.x >> 5) {
-            const int c = r / (L.jy * L.jz), rr = r - c * (L.jy * L.jz);
-            const int d = rr / L.jy, b = rr - d * L.jy;
-            const F *srow = jt + (size_t)c * L.JV + (d * L.jy + b) * L.jx;
-            F *drow = (F *)fp.J[c] + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
-            for (int a = lane; a < L.jx; a += 32) {
-                const F v = srow[a];
-                if (v != F(0)) atomicAdd(drow + wjx[a], v);
+        const int total = 3 * L.JV, nth = blockDim.x, jxy = L.jx * L.jy;
+        for (int i = t; i < total; i += nth) {
+            const F v = jt[i];
+            if (v != F(0)) {
+                const int c = i / L.JV, r = i - c * L.JV;
+                const int d = r / jxy, r2 = r - d * jxy;
+                const int b = r2 / L.jx, a = r2 - b * L.jx;
+                atomicAdd((F *)fp.J[c] + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx + wjx[a], v);
             }
         }
     }

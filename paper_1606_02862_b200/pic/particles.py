@@ -50,11 +50,13 @@ GROW_AT = 0.85
 def initial_frames(max_col: int, mean_col: float) -> int:
     """Frames per super cell for a fresh store: room for the fullest cell
     and for the spread a thermal plasma develops (cell counts drift towards
-    Poisson statistics; the fullest of ~10^7 cells sits ~5.5 sigma above the
-    mean), with margin so that growth -- a repack plus large allocations --
-    stays out of steady-state stepping."""
+    Poisson statistics, and the fullest of ~10^6-10^7 cells in a thermal
+    plasma has been measured 6.5 sigma above the mean -- 57-60 particles at
+    25 ppc, tools/occupancy_trace.py), with margin so that growth -- a
+    repack plus large allocations -- stays out of steady-state stepping.
+    The store is a few GB against 180 GB of HBM: spend memory, not time."""
     return max(8, math.ceil(max_col * 1.3) + 4,
-               math.ceil(mean_col + 7.0 * math.sqrt(max(mean_col, 1.0))) + 8)
+               math.ceil(mean_col + 10.0 * math.sqrt(max(mean_col, 1.0))) + 8)
 
 
 class _Columns:
@@ -207,11 +209,27 @@ class SuperCellStore:
         return self.count.cpu().numpy().astype(np.int64)
 
     # -- host <-> device ------------------------------------------------------------
-    def packed(self, fields=PACKED_FIELDS, stream=None) -> dict:
+    def packed(self, fields=PACKED_FIELDS, stream=None, out=None) -> dict:
         """Canonical-order records (super cell, cell, frame) as host numpy
-        arrays: global cells int32, storage-type floats (export kernel)."""
-        out = self.packed_device(stream)
-        return {n: out[n].cpu().numpy() for n in fields}
+        arrays: global cells int32, storage-type floats (export kernel).
+        `out` (optional): dict of preallocated host tensors (pinned for an
+        asynchronous DMA) with at least census() elements each; the result
+        arrays are views of them."""
+        dev = self.packed_device(stream)
+        if out is None:
+            return {n: dev[n].cpu().numpy() for n in fields}
+        n = dev["cx"].shape[0]
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        res = {}
+        with torch.cuda.stream(s):
+            for f in fields:
+                dst = out[f]
+                if dst.numel() < n:
+                    raise ValueError(f"packed: out[{f!r}] holds {dst.numel()} < {n} records")
+                dst[:n].copy_(dev[f], non_blocking=True)
+                res[f] = dst[:n]
+        s.synchronize()
+        return {f: v.numpy() for f, v in res.items()}
 
     def packed_device(self, stream=None, columns=None, clear=False) -> dict:
         """Export (device tensors) the particles of all columns, or of the
