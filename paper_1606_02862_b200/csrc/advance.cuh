@@ -16,6 +16,8 @@
 //   queue kWarps x kWarpQ crossing records    (per warp, deposited after the
 //                                             main loop: no block barriers)
 //   arr   V int                               in-super-cell arrivals per cell
+//   pf    2 x 7 x 256 F                       next-particle records, cp.async
+//                                             (no registers held between rounds)
 //   wrap  periodic index tables for staging and the J flush
 
 struct FieldPtrs {
@@ -37,9 +39,21 @@ __host__ __device__ constexpr double stagger(int c, int a) {
                     : (a == 2 ? 0.5 : 1.0);
 }
 
+// 4/8-byte asynchronous global -> shared copy (LDGSTS), bypassing registers.
+template <typename F>
+__device__ __forceinline__ void cp_async_elem(F *dst, const F *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(d), "l"(src),
+                 "n"((int)sizeof(F)));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 struct AdvLayout {
     int tx, ty, tz, TV, jx, jy, jz, JV;
-    size_t off_jt, off_qf, off_qi, off_arr, off_wrap, bytes;
+    size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, bytes;
 };
 
 template <typename F, int ORDER>
@@ -58,6 +72,8 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     o += (size_t)kWarps * kWarpQ * sizeof(int);
     L.off_arr = o;
     o += (size_t)kMaxCells * sizeof(int);
+    L.off_pf = o;
+    o += (size_t)2 * 7 * kMaxCells * sizeof(F);   // double-buffered next-particle records
     L.off_wrap = o;
     o += (size_t)(L.tx + L.ty + L.tz + L.jx + L.jy + L.jz) * sizeof(int);
     L.bytes = (o + 15) & ~size_t(15);
@@ -159,7 +175,7 @@ __device__ __noinline__ void deposit_cross(F *__restrict__ jt, int jx, int jy, i
         for (int j1 = 1; j1 <= NS; ++j1) {
             if (j1 > nt[a1]) continue;
             const CT u = s0[a1][j1 - 1] + CT(0.5) * ds[a1][j1 - 1];
-            const CT v = CT(0.5) * s0[a1][j1 - 1] + ds[a1][j1 - 1] / CT(3);
+            const CT v = CT(0.5) * s0[a1][j1 - 1] + ds[a1][j1 - 1] * CT(1.0 / 3.0);
 #pragma unroll
             for (int j2 = 1; j2 <= NS; ++j2) {
                 if (j2 > nt[a2]) continue;
@@ -230,7 +246,7 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
         P[2] = fw * ((dsc[0] + dsc[1]) + dsc[2]);
 #pragma unroll
         for (int j1 = 0; j1 < 3; ++j1) {
-            const CT u = s0p[j1] + CT(0.5) * dsp[j1], v = CT(0.5) * s0p[j1] + dsp[j1] / CT(3);
+            const CT u = s0p[j1] + CT(0.5) * dsp[j1], v = CT(0.5) * s0p[j1] + dsp[j1] * CT(1.0 / 3.0);
 #pragma unroll
             for (int j2 = 0; j2 < 3; ++j2) {
                 const CT T = u * s0q[j2] + v * dsq[j2];
@@ -252,7 +268,7 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
         const CT P0 = fw * dsa[0], P1 = fw * (dsa[0] + dsa[1]);
 #pragma unroll
         for (int j1 = 0; j1 < 4; ++j1) {
-            const CT u = s0c[j1] + CT(0.5) * dsc[j1], v = CT(0.5) * s0c[j1] + dsc[j1] / CT(3);
+            const CT u = s0c[j1] + CT(0.5) * dsc[j1], v = CT(0.5) * s0c[j1] + dsc[j1] * CT(1.0 / 3.0);
 #pragma unroll
             for (int j2 = 0; j2 < 3; ++j2) {
                 const CT T = u * s0o[j2] + v * dso[j2];
@@ -412,7 +428,11 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                     const int c = i / L.TV, r = i - c * L.TV;
                     const int d = r / txy_, r2 = r - d * txy_;
                     const int b = r2 / L.tx, a = r2 - b * L.tx;
-                    const F *src = (const F *)(c < 3 ? fp.E[c] : fp.B[c - 3]);
+                    // select chain, not fp.E[c]: a runtime index into the
+                    // parameter struct would copy it to local memory
+                    const void *sv = c == 0 ? fp.E[0] : c == 1 ? fp.E[1] : c == 2 ? fp.E[2]
+                                   : c == 3 ? fp.B[0] : c == 4 ? fp.B[1] : fp.B[2];
+                    const F *src = (const F *)sv;
                     v[u] = __ldg(src + ((int64_t)wtz[d] * g.ny + wty[b]) * g.nx + wtx[a]);
                 }
             }
@@ -463,17 +483,29 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     int n_err = 0;
     int wq = 0;      // this warp's queue fill (warp-uniform)
 
-    // software prefetch of the next particle's record
-    F pox = 0, poy = 0, poz = 0, pux = 0, puy = 0, puz = 0, pw = 0;
     auto slot_of = [&](int i) -> int64_t {
         const int k = i < front_in ? i : K - back_in + (i - front_in);
         return ((int64_t)sc * K + k) * V + t;
     };
-    if (0 < n_t) {
-        const int64_t q = slot_of(0);
-        pox = in.ox[q]; poy = in.oy[q]; poz = in.oz[q];
-        pux = in.ux[q]; puy = in.uy[q]; puz = in.uz[q]; pw = in.w[q];
-    }
+    // next-particle records are copied global -> shared asynchronously
+    // (double buffered, this thread's slots only) and read at their uses,
+    // so they occupy no registers between rounds
+    F *pf = reinterpret_cast<F *>(smem_raw + L.off_pf) + t;
+    auto prefetch = [&](int i) {
+        if (i < n_t) {
+            const int64_t q = slot_of(i);
+            F *d = pf + (i & 1) * 7 * kMaxCells;
+            cp_async_elem(d + 0 * kMaxCells, in.ox + q);
+            cp_async_elem(d + 1 * kMaxCells, in.oy + q);
+            cp_async_elem(d + 2 * kMaxCells, in.oz + q);
+            cp_async_elem(d + 3 * kMaxCells, in.ux + q);
+            cp_async_elem(d + 4 * kMaxCells, in.uy + q);
+            cp_async_elem(d + 5 * kMaxCells, in.uz + q);
+            cp_async_elem(d + 6 * kMaxCells, in.w + q);
+        }
+        cp_async_commit();
+    };
+    prefetch(0);
 
     // Deposit the queued crossing particles of this warp (lanes take one
     // record each; CAS into the J tile).
@@ -503,12 +535,12 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
     for (int i = 0; i < n_w; ++i) {
         const bool active = i < n_t;
-        const F ox = pox, oy = poy, oz = poz, ux = pux, uy = puy, uz = puz, w = pw;
-        if (i + 1 < n_t) {
-            const int64_t q = slot_of(i + 1);
-            pox = in.ox[q]; poy = in.oy[q]; poz = in.oz[q];
-            pux = in.ux[q]; puy = in.uy[q]; puz = in.uz[q]; pw = in.w[q];
-        }
+        cp_async_wait_all();
+        const F *cur = pf + (i & 1) * 7 * kMaxCells;
+        prefetch(i + 1);
+        const F &ox = cur[0 * kMaxCells], &oy = cur[1 * kMaxCells], &oz = cur[2 * kMaxCells],
+                &ux = cur[3 * kMaxCells], &uy = cur[4 * kMaxCells], &uz = cur[5 * kMaxCells],
+                &w = cur[6 * kMaxCells];
         bool queue = false, leave = false, mover = false, stay = false;
         F nox = 0, noy = 0, noz = 0, nux = 0, nuy = 0, nuz = 0;
         int dcx = 0, dcy = 0, dcz = 0, ncx = 0, ncy = 0, ncz = 0, dest = 0, nlc = 0;
@@ -695,7 +727,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 const int c = i / L.JV, r = i - c * L.JV;
                 const int d = r / jxy, r2 = r - d * jxy;
                 const int b = r2 / L.jx, a = r2 - b * L.jx;
-                atomicAdd((F *)fp.J[c] + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx + wjx[a], v);
+                F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
+                atomicAdd(dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx + wjx[a], v);
             }
         }
     }
