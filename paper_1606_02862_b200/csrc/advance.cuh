@@ -693,23 +693,25 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     // ---- reduce the register accumulators into the J tile ----------------
     // Sweep s adds accumulator s of every cell: the targets cell + offset(s)
     // are distinct across threads, so plain read-modify-writes are race free;
-    // the barrier orders consecutive sweeps.
+    // the three components go to different arrays and share a sweep (18
+    // sweeps); the barrier orders consecutive sweeps.
     if (REGACC) {
         F *Jb = jt + ((lz * L.jy) + ly) * L.jx + lx;
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-            for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 3; ++b)
 #pragma unroll
-                for (int b = 0; b < 3; ++b)
+                for (int d = 0; d < 3; ++d) {
+                    if (owner) {
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        if (owner) {
+                        for (int c = 0; c < 3; ++c) {
                             F *p = Jb + c * L.JV + regacc_offset(c, a + 1, b + 1, d + 1, L.jx, L.jy);
                             *p = *p + (F)R.a[c][a][b][d];
                         }
-                        __syncthreads();
                     }
+                    __syncthreads();
+                }
     }
 
     // ---- deposit the crossing particles queued during the loop -----------
