@@ -196,6 +196,185 @@ __device__ __noinline__ void deposit_cross(F *__restrict__ jt, int jx, int jy, i
     }
 }
 
+// Compact form of deposit_cross for the kernels that queue every particle
+// (PCS, float64): the component and transverse-row loops are NOT unrolled
+// -- the per-axis register arrays are rotated instead, so every index stays
+// a compile-time constant (no local memory) while the code is ~NS x NA CAS
+// sites instead of 3 x NS x NS x NA (the unrolled PCS routine is ~90 KB of
+// SASS and stalls on instruction fetch).  Same arithmetic and order.
+template <typename F, int ORDER>
+__device__ __noinline__ void deposit_cross_compact(F *__restrict__ jt, int jx, int jy, int JV,
+                                                   int lx, int ly, int lz, int dcx, int dcy,
+                                                   int dcz, F oox, F ooy, F ooz, F nox, F noy,
+                                                   F noz, F w, double fac0, double fac1,
+                                                   double fac2) {
+    using CT = F;
+    constexpr int NP = Shape<ORDER>::NP, NS = NP - 1, NA = NP - 2;
+    const int dc[3] = {dcx, dcy, dcz};
+    const F oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
+    const double fac[3] = {fac0, fac1, fac2};
+    CT s0[3][NS], ds[3][NS], P[3][NA];
+    int nt[3], na[3], st[3] = {1, jx, jx * jy};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int m = dc[a] < 0 ? -1 : 0;
+        CT s1[NS];
+        shape_anchor<ORDER, CT>((CT)oo[a] - (CT)m, s0[a]);
+        shape_anchor<ORDER, CT>((CT)no[a] + (CT)(dc[a] - m), s1);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) ds[a][i] = s1[i] - s0[a][i];
+        nt[a] = dc[a] != 0 ? NS : NS - 1;
+        na[a] = dc[a] != 0 ? NA : NA - 1;
+        const CT fw = (CT)(fac[a] * (double)w);
+        CT run = CT(0);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) { run += ds[a][i]; P[a][i] = fw * run; }
+    }
+    const int ax = lx + min(dcx, 0), ay = ly + min(dcy, 0), az = lz + min(dcz, 0);
+    F *Jc = jt + (az * jy + ay) * jx + ax;
+    // invariant: slot 0 = the component's axis, 1 = first transverse, 2 = second
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) {
+        CT u1[NS], v1[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            u1[j] = s0[1][j] + CT(0.5) * ds[1][j];
+            v1[j] = CT(0.5) * s0[1][j] + ds[1][j] * CT(1.0 / 3.0);
+        }
+        const int sa = st[0], s1_ = st[1], s2_ = st[2], nt1 = nt[1], nt2 = nt[2], nac = na[0];
+        F *row = Jc + s1_;
+#pragma unroll 1
+        for (int j1 = 0; j1 < nt1; ++j1) {
+            const CT uu = u1[0], vv = v1[0];
+#pragma unroll
+            for (int j2 = 0; j2 < NS; ++j2) {
+                if (j2 < nt2) {
+                    const CT T = uu * s0[2][j2] + vv * ds[2][j2];
+                    if (T != CT(0)) {
+                        F *q = row + (j2 + 1) * s2_;
+#pragma unroll
+                        for (int ja = 0; ja < NA; ++ja) {
+                            const CT val = P[0][ja] * T;
+                            if (ja < nac && val != CT(0)) atomicAdd(q + (ja + 1) * sa, (F)val);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j + 1 < NS; ++j) { u1[j] = u1[j + 1]; v1[j] = v1[j + 1]; }
+            row += s1_;
+        }
+        Jc += JV;
+        // rotate the axes: (c, c+1, c+2) -> (c+1, c+2, c+3)
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            const CT a0 = s0[0][j], b0 = ds[0][j];
+            s0[0][j] = s0[1][j]; s0[1][j] = s0[2][j]; s0[2][j] = a0;
+            ds[0][j] = ds[1][j]; ds[1][j] = ds[2][j]; ds[2][j] = b0;
+        }
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+            const CT p0 = P[0][j];
+            P[0][j] = P[1][j]; P[1][j] = P[2][j]; P[2][j] = p0;
+        }
+        { const int t0 = nt[0]; nt[0] = nt[1]; nt[1] = nt[2]; nt[2] = t0; }
+        { const int t0 = na[0]; na[0] = na[1]; na[1] = na[2]; na[2] = t0; }
+        { const int t0 = st[0]; st[0] = st[1]; st[1] = st[2]; st[2] = t0; }
+    }
+}
+
+// Warp-cooperative form of deposit_cross, for the rare particles that cross
+// faces on more than one axis in the register-deposit kernels: all 32
+// lanes take the same record.  Lanes 0..3*NS-1 evaluate one support point
+// (axis a, index i) each -- s0, ds, the transverse factors u, v and the
+// along-axis running sum P (segmented shuffle scan) -- and the footprint
+// entries (component c, along ja, transverse j1, j2) are then dealt out 32
+// per pass, each lane fetching its operands by shuffle and issuing one CAS.
+// Distinct lanes hit distinct entries, the code is a few hundred bytes (the
+// fully unrolled per-lane PCS routine is ~90 KB and thrashes the instruction
+// cache) and every lane is busy.  Same arithmetic as deposit_cross up to the
+// summation order of P (J is compared within tolerance).
+template <int ORDER, typename CT>
+__device__ __forceinline__ CT shape_point(CT x, int i) {
+    constexpr int H = Shape<ORDER>::H;
+    CT d = x - (CT)((double)(i + 1 - H) + 0.5);
+    d = d < CT(0) ? -d : d;
+    if (ORDER == 2) {
+        const CT e = CT(1.5) - d;
+        return d < CT(0.5) ? CT(0.75) - d * d : (d < CT(1.5) ? CT(0.5) * e * e : CT(0));
+    } else if (ORDER == 1) {
+        return d < CT(1) ? CT(1) - d : CT(0);
+    } else {
+        const CT e = CT(2) - d;
+        return d < CT(1) ? (CT(4) - CT(6) * d * d + CT(3) * d * d * d) / CT(6)
+                         : (d < CT(2) ? e * e * e / CT(6) : CT(0));
+    }
+}
+
+template <typename F, int ORDER>
+__device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, int JV, int lane,
+                                          int lx, int ly, int lz, int dcx, int dcy, int dcz,
+                                          F oox, F ooy, F ooz, F nox, F noy, F noz, F w,
+                                          double fac0, double fac1, double fac2) {
+    using CT = F;
+    constexpr int NP = Shape<ORDER>::NP, NS = NP - 1, NA = NP - 2;
+    constexpr unsigned FULL = 0xffffffffu;
+    // this lane's support point
+    const int a = lane / NS, i = lane - a * NS;
+    const int dca = a == 0 ? dcx : a == 1 ? dcy : dcz;
+    const F ooa = a == 0 ? oox : a == 1 ? ooy : ooz;
+    const F noa = a == 0 ? nox : a == 1 ? noy : noz;
+    const double faca = a == 0 ? fac0 : a == 1 ? fac1 : fac2;
+    const int m = dca < 0 ? -1 : 0;
+    const CT s0 = shape_point<ORDER, CT>((CT)ooa - (CT)m, i);
+    const CT ds = shape_point<ORDER, CT>((CT)noa + (CT)(dca - m), i) - s0;
+    const CT u = s0 + CT(0.5) * ds, v = CT(0.5) * s0 + ds * CT(1.0 / 3.0);
+    CT run = ds;
+#pragma unroll
+    for (int o = 1; o < NS; o <<= 1) {
+        const CT y = __shfl_up_sync(FULL, run, o);
+        if (i >= o) run += y;
+    }
+    const CT P = (CT)(faca * (double)w) * run;
+    const int ntx = dcx ? NS : NS - 1, nty = dcy ? NS : NS - 1, ntz = dcz ? NS : NS - 1;
+    const int ax = lx + min(dcx, 0), ay = ly + min(dcy, 0), az = lz + min(dcz, 0);
+    F *base = jt + (az * jy + ay) * jx + ax;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
+        const int dcc = c == 0 ? dcx : c == 1 ? dcy : dcz;
+        const int nt1 = a1 == 0 ? ntx : a1 == 1 ? nty : ntz;
+        const int nt2 = a2 == 0 ? ntx : a2 == 1 ? nty : ntz;
+        const int na = dcc ? NA : NA - 1;
+        const int per_a = nt1 * nt2, npts = na * per_a;
+        // x / d for x < 2^10, d <= 64 (exact): multiply by ceil(2^16 / d)
+        const unsigned r_pa = 65536u / per_a + 1u, r_n2 = 65536u / nt2 + 1u;
+        F *Jc = base + c * JV;
+        for (int p0 = 0; p0 < npts; p0 += 32) {   // warp-uniform passes
+            const int p = p0 + lane;
+            const int ja = (int)(((unsigned)p * r_pa) >> 16);
+            const int rem = p - ja * per_a;
+            const int j1 = (int)(((unsigned)rem * r_n2) >> 16), j2 = rem - j1 * nt2;
+            const CT u1 = __shfl_sync(FULL, u, a1 * NS + j1);
+            const CT v1 = __shfl_sync(FULL, v, a1 * NS + j1);
+            const CT s02 = __shfl_sync(FULL, s0, a2 * NS + j2);
+            const CT ds2 = __shfl_sync(FULL, ds, a2 * NS + j2);
+            const CT Pv = __shfl_sync(FULL, P, c * NS + ja);
+            if (p < npts) {
+                const CT T = u1 * s02 + v1 * ds2;
+                const CT val = Pv * T;
+                if (T != CT(0) && val != CT(0)) {
+                    int o;
+                    if (c == 0) o = ((j2 + 1) * jy + (j1 + 1)) * jx + (ja + 1);
+                    else if (c == 1) o = ((j1 + 1) * jy + (ja + 1)) * jx + (j2 + 1);
+                    else o = ((ja + 1) * jy + (j2 + 1)) * jx + (j1 + 1);
+                    atomicAdd(Jc + o, (F)val);
+                }
+            }
+        }
+    }
+}
+
 // Deposit of a particle that crossed exactly one cell face, along axis k
 // (the common case: a two-axis crossing is ~40x rarer).  Axes are rotated so
 // the crossing axis is A0; with the anchor min(old, new) its supports span
@@ -510,28 +689,70 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     // Deposit the queued crossing particles of this warp (lanes take one
     // record each; CAS into the J tile).
     auto drain_queue = [&]() {
-            __syncwarp();
+        __syncwarp();
+        auto warp_record = [&](int j) {   // warp-uniform j
+            const int info = q_info[j];
+            deposit_warp<F, ORDER>(jt, L.jx, L.jy, L.JV, lane, info & 255, (info >> 8) & 255,
+                                   (info >> 16) & 255, ((info >> 24) & 3) - 1,
+                                   ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
+                                   q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
+                                   q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
+                                   q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+        };
+        if (!REGACC) {
+            // PCS / float64: every particle is queued; one record per lane
+            // (PCS: the compact routine -- its unrolled form does not fit
+            // the instruction cache; CIC/TSC: unrolled)
             for (int j = lane; j < wq; j += 32) {
                 const int info = q_info[j];
                 const int qx = info & 255, qy = (info >> 8) & 255, qz = (info >> 16) & 255;
                 const int ddx = ((info >> 24) & 3) - 1, ddy = ((info >> 26) & 3) - 1,
                           ddz = ((info >> 28) & 3) - 1;
-                const int ncross = (ddx != 0) + (ddy != 0) + (ddz != 0);
-                if (ORDER != 3 && ncross == 1) {
-                    const int k = ddx ? 0 : (ddy ? 1 : 2);
-                    deposit_cross1<F, ORDER>(jt, L.jx, L.jy, L.JV, k, qx, qy, qz, ddx + ddy + ddz,
-                                             q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
-                                             q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                             q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
-                } else {
-                    deposit_cross<F, ORDER, F>(jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz,
-                                               q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
-                                               q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                               q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                if (ORDER == 3)
+                    deposit_cross_compact<F, ORDER>(
+                        jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz, q_f[0 * QS + j],
+                        q_f[1 * QS + j], q_f[2 * QS + j], q_f[3 * QS + j], q_f[4 * QS + j],
+                        q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                else
+                    deposit_cross<F, ORDER, F>(
+                        jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz, q_f[0 * QS + j],
+                        q_f[1 * QS + j], q_f[2 * QS + j], q_f[3 * QS + j], q_f[4 * QS + j],
+                        q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+            }
+        } else {
+            // single-axis crossers (the common case): one record per lane,
+            // anchor-shifted fp32 routine; the rare multi-axis ones: one warp
+            // per record
+            for (int j0 = 0; j0 < wq; j0 += 32) {
+                const int j = j0 + lane;
+                bool multi = false;
+                if (j < wq) {
+                    const int info = q_info[j];
+                    const int ddx = ((info >> 24) & 3) - 1, ddy = ((info >> 26) & 3) - 1,
+                              ddz = ((info >> 28) & 3) - 1;
+                    if ((ddx != 0) + (ddy != 0) + (ddz != 0) == 1) {
+                        const int k = ddx ? 0 : (ddy ? 1 : 2);
+                        deposit_cross1<F, ORDER>(jt, L.jx, L.jy, L.JV, k, info & 255,
+                                                 (info >> 8) & 255, (info >> 16) & 255,
+                                                 ddx + ddy + ddz, q_f[0 * QS + j],
+                                                 q_f[1 * QS + j], q_f[2 * QS + j],
+                                                 q_f[3 * QS + j], q_f[4 * QS + j],
+                                                 q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0],
+                                                 sp.fac[1], sp.fac[2]);
+                    } else {
+                        multi = true;
+                    }
+                }
+                unsigned mm = __ballot_sync(0xffffffffu, multi);
+                while (mm) {
+                    const int b = __ffs(mm) - 1;
+                    mm &= mm - 1u;
+                    warp_record(j0 + b);
                 }
             }
-            __syncwarp();
-            };
+        }
+        __syncwarp();
+    };
 
     for (int i = 0; i < n_w; ++i) {
         const bool active = i < n_t;
