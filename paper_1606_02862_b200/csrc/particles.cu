@@ -40,6 +40,7 @@ __global__ void shift_kernel(StoreT<F> out, ExchT<F> ex, Geo g, int32_t *__restr
     if (n > ex.capacity) n = ex.capacity;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&status[KWB_ST_LEAVERS], n);
     const int V = g.scx * g.scy * g.scz, K = out.frames;
+    int fill_max = 0;   // warp-aggregated: one same-address atomicMax per warp, not per record
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int d = ex.dest[i];
         const int bx = d % g.gx, by = (d / g.gx) % g.gy, bz = d / (g.gx * g.gy);
@@ -53,12 +54,14 @@ __global__ void shift_kernel(StoreT<F> out, ExchT<F> ex, Geo g, int32_t *__restr
             atomicAdd(&status[KWB_ST_STORE_OVERFLOW], 1);
             continue;
         }
-        atomicMax(&status[KWB_ST_MAX_COUNT], fill);
+        fill_max = max(fill_max, fill);
         const int64_t o = ((int64_t)d * K + (K - 1 - slot)) * V + c;
         out.ox[o] = ex.ox[i]; out.oy[o] = ex.oy[i]; out.oz[o] = ex.oz[i];
         out.ux[o] = ex.ux[i]; out.uy[o] = ex.uy[i]; out.uz[o] = ex.uz[i];
         out.w[o] = ex.w[i];
     }
+    fill_max = __reduce_max_sync(0xffffffffu, fill_max);
+    if ((threadIdx.x & 31) == 0 && fill_max > 0) atomicMax(&status[KWB_ST_MAX_COUNT], fill_max);
 }
 
 // ---- store load / export / repack ---------------------------------------
