@@ -873,16 +873,17 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         }
 
         // ---- write the particle to its column / the exchange --------------
-        if (stay) {
-            const int64_t o = ((int64_t)sc * K + fo) * V + t;
-            ++fo;
-            out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
-            out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
-            out.w[o] = w;
-        } else if (mover) {
-            const int slot = atomicAdd(&arr[nlc], 1);
-            if (slot < K) {
-                const int64_t o = ((int64_t)sc * K + (K - 1 - slot)) * V + nlc;
+        {   // one store block for stayers (own column front) and in-super-cell
+            // movers (destination column back): less code, fewer reconvergence points
+            int frame = -1, cell = t;
+            if (stay) {
+                frame = fo++;
+            } else if (mover) {
+                const int slot = atomicAdd(&arr[nlc], 1);
+                if (slot < K) { frame = K - 1 - slot; cell = nlc; }
+            }
+            if (frame >= 0) {
+                const int64_t o = ((int64_t)sc * K + frame) * V + cell;
                 out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
                 out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
                 out.w[o] = w;
