@@ -484,9 +484,50 @@ __device__ __forceinline__ void shape123f(float x, float (&s)[3]) {
 // factor, factorised).  The closing entry ja = 3 is sum(s1) - sum(s0), a
 // rounding residue, and is dropped.  fp32 with FMA: J is compared within
 // tolerance, never bitwise (the reference's own J order is not fixed).
+// The (ja = 1, ja = 2) pair of an entry shares T: one packed FFMA2
+// (fma.rn.f32x2, sm_100) updates both -- the same two round-to-nearest FMAs.
+#ifndef KWB_NO_FFMA2
+struct RegAcc {
+    unsigned long long p[3][3][3];  // [component][j1-1][j2-1] = {ja=1, ja=2} as f32x2
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) p[c][b][d] = 0ull;
+    }
+    __device__ __forceinline__ float get(int c, int a, int b, int d) const {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p[c][b][d]));
+        return a == 0 ? lo : hi;
+    }
+    __device__ __forceinline__ static unsigned long long pack(float lo, float hi) {
+        unsigned long long r;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+        return r;
+    }
+    __device__ __forceinline__ void fma2(int c, int b, int d, unsigned long long P, float T) {
+        const unsigned long long TT = pack(T, T);   // folded into FFMA2's scalar operand
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(p[c][b][d]) : "l"(P), "l"(TT));
+    }
+};
+#else
 struct RegAcc {
     float a[3][2][3][3];  // [component][ja-1][j1-1][j2-1]
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a_ = 0; a_ < 2; ++a_)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) a[c][a_][b][d] = 0.f;
+    }
+    __device__ __forceinline__ float get(int c, int a_, int b, int d) const { return a[c][a_][b][d]; }
 };
+#endif
 
 template <int ORDER>
 __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, float ooz,
@@ -514,6 +555,9 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
         const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;  // transverse axes: x:(y,z) y:(z,x) z:(x,y)
         const float p1 = __fmul_rn(fw[c], ds[c][0]);
         const float p2 = __fmul_rn(fw[c], __fadd_rn(ds[c][0], ds[c][1]));
+#ifndef KWB_NO_FFMA2
+        const unsigned long long P12 = RegAcc::pack(p1, p2);
+#endif
 #pragma unroll
         for (int j1 = 0; j1 < 3; ++j1) {
             const float u = __fmaf_rn(0.5f, ds[a1][j1], s0[a1][j1]);
@@ -521,8 +565,12 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
 #pragma unroll
             for (int j2 = 0; j2 < 3; ++j2) {
                 const float T = __fmaf_rn(u, s0[a2][j2], __fmul_rn(v, ds[a2][j2]));
+#ifndef KWB_NO_FFMA2
+                R.fma2(c, j1, j2, P12, T);
+#else
                 R.a[c][0][j1][j2] = __fmaf_rn(p1, T, R.a[c][0][j1][j2]);
                 R.a[c][1][j1][j2] = __fmaf_rn(p2, T, R.a[c][1][j1][j2]);
+#endif
             }
         }
     }
@@ -642,16 +690,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     __syncthreads();
 
     RegAcc R;
-    if (REGACC) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) R.a[c][a][b][d] = 0.f;
-    }
+    if (REGACC) R.zero();
     const double qm = sp.qm_half_dt;
     const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
     const double cxd = (double)cx, cyd = (double)cy, czd = (double)cz;
@@ -929,7 +968,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             F *p = Jb + c * L.JV + regacc_offset(c, a + 1, b + 1, d + 1, L.jx, L.jy);
-                            *p = *p + (F)R.a[c][a][b][d];
+                            *p = *p + (F)R.get(c, a, b, d);
                         }
                     }
                     __syncthreads();
