@@ -83,6 +83,8 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
 // Trilinear sample of one staged (float64) component, pic/kernels.py:26-47.
 // Tile origin = super-cell origin - 1.  The floor/fraction of an axis is
 // shared by every component with the same stagger on that axis (CSE).
+// All eight corner loads are issued before the arithmetic (measured: the
+// compiler then overlaps them with the other components' math).
 template <int C>
 __device__ __forceinline__ double sample_tile(const double *__restrict__ T, double px, double py,
                                               double pz, int ox0, int oy0, int oz0, int tx,
@@ -90,15 +92,15 @@ __device__ __forceinline__ double sample_tile(const double *__restrict__ T, doub
     const double ttx = px - stagger(C, 0), tty = py - stagger(C, 1), ttz = pz - stagger(C, 2);
     const int ix = (int)floor(ttx), iy = (int)floor(tty), iz = (int)floor(ttz);
     const double fx = ttx - (double)ix, fy = tty - (double)iy, fz = ttz - (double)iz;
-    const double *r00 = T + (iz - oz0) * txy + (iy - oy0) * tx + (ix - ox0);
-    const double *r10 = r00 + tx;
-    const double *r01 = r00 + txy;
-    const double *r11 = r01 + tx;
+    const int i00 = (iz - oz0) * txy + (iy - oy0) * tx + (ix - ox0);
+    const double *r00 = T + i00, *r10 = r00 + tx, *r01 = r00 + txy, *r11 = r01 + tx;
+    const double a00 = r00[0], b00 = r00[1], a10 = r10[0], b10 = r10[1];   // (x, x+1) corners
+    const double a01 = r01[0], b01 = r01[1], a11 = r11[0], b11 = r11[1];
     const double gx = 1.0 - fx;
-    const double c00 = r00[0] * gx + r00[1] * fx;
-    const double c10 = r10[0] * gx + r10[1] * fx;
-    const double c01 = r01[0] * gx + r01[1] * fx;
-    const double c11 = r11[0] * gx + r11[1] * fx;
+    const double c00 = a00 * gx + b00 * fx;
+    const double c10 = a10 * gx + b10 * fx;
+    const double c01 = a01 * gx + b01 * fx;
+    const double c11 = a11 * gx + b11 * fx;
     return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz;
 }
 
@@ -639,7 +641,6 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     if (t == 0) s_maxcol = 0;
     for (int i = t; i < 3 * L.JV; i += blockDim.x) jt[i] = F(0);
     __syncthreads();
-#ifndef KWB_EXP_ROWSTAGE
     {
         // flat over (component, z, y, x) so every lane works, and batches of
         // kStageB independent loads in flight per thread (one memory latency
@@ -670,19 +671,6 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             }
         }
     }
-#else
-    {
-        const int rows = 6 * L.ty * L.tz;  // (component, z, y) rows of tx cells
-        for (int r = wid; r < rows; r += blockDim.x >> 5) {
-            const int c = r / (L.ty * L.tz), rr = r - c * (L.ty * L.tz);
-            const int d = rr / L.ty, b = rr - d * L.ty;
-            const F *src = (const F *)(c < 3 ? fp.E[c] : fp.B[c - 3]) +
-                           ((int64_t)wtz[d] * g.ny + wty[b]) * g.nx;
-            double *dst = ebd + (size_t)c * L.TV + (d * L.ty + b) * L.tx;
-            for (int a = lane; a < L.tx; a += 32) dst[a] = (double)src[wtx[a]];
-        }
-    }
-#endif
 
     int n_w = n_t;  // warp-uniform trip count
 #pragma unroll
