@@ -17,7 +17,7 @@
  *   kwb_particle_moments / kwb_field_stats
  *                          <- Simulation.diagnostics pic/sim.py:191-225
  *   kwb_init_khi           <- init_khi (on-device path)  pic/sim.py:239-302
- *   kwb_store_load / kwb_store_export
+ *   kwb_store_load / kwb_store_export (+ _counted / kwb_store_extract)
  *                          <- _bulk_fill / SuperCellStore.packed
  *                             pic/sim.py:305-328, pic/particles.py:174-186
  *
@@ -68,6 +68,7 @@ extern "C" {
 #define KWB_ST_LEAVERS 3       /* leavers summed over species this step */
 #define KWB_ST_MAX_COUNT 4     /* max particles in one cell column after the shift */
 #define KWB_ST_LOAD_ERRORS 5   /* kwb_store_load records that did not fit */
+#define KWB_ST_GUARD_OVERFLOW 6/* kwb_store_extract records beyond the message capacity */
 #define KWB_STATUS_WORDS 8
 
 typedef struct CUstream_st *kwb_stream_t;
@@ -177,6 +178,25 @@ int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
 int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin, int64_t col_end,
                      const int64_t *cell_start, int clear, int32_t *cx, int32_t *cy, int32_t *cz,
                      void *const f7[7], kwb_stream_t stream);
+
+/* Bounded, host-synchronisation-free form of kwb_store_export with clear:
+ * if the range holds at most `capacity` records (total read on the device
+ * from cell_start[col_end - col_begin]) they are exported and the columns
+ * emptied, and *count_out (device) = the total; otherwise nothing is
+ * exported or cleared, *count_out = 0 and status[KWB_ST_GUARD_OVERFLOW]
+ * counts the excess.  The z-slab decomposition ships guard-layer particles
+ * in fixed-capacity messages this way. */
+int kwb_store_extract(const kwb_grid *g, const kwb_store *st, int64_t col_begin,
+                      int64_t col_end, const int64_t *cell_start, int64_t capacity,
+                      int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
+                      int64_t *count_out, int32_t *status, kwb_stream_t stream);
+
+/* kwb_store_load with the record count on the device: appends
+ * min(*n_dev, capacity) records. */
+int kwb_store_load_counted(const kwb_grid *g, const kwb_store *st, const int64_t *n_dev,
+                           int64_t capacity, const int32_t *cx, const int32_t *cy,
+                           const int32_t *cz, void *const f7[7], int32_t *status,
+                           kwb_stream_t stream);
 
 /* On-device KHI/thermal start (pic/sim.py:239-302 semantics, Philox jitter):
  * fills every cell column with the ppc quiet-start particles of the species.

@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("KWB_LIB_PATH") or os.path.join(_HERE, "libkwb200.so")
 
 KWB_F32, KWB_F64 = 0, 1
 ST_MOVE_ERRORS, ST_EXCH_OVERFLOW, ST_STORE_OVERFLOW, ST_LEAVERS, ST_MAX_COUNT, \
-    ST_LOAD_ERRORS = range(6)
+    ST_LOAD_ERRORS, ST_GUARD_OVERFLOW = range(7)
 STATUS_WORDS = 8
 
 P = ctypes.c_void_p
@@ -75,6 +75,8 @@ _SIGS = {
     "kwb_field_stats": ([P, Ptr3, Ptr3, P, P], ctypes.c_int),
     "kwb_store_load": ([P, P, I64, P, P, P, Ptr7, P, P], ctypes.c_int),
     "kwb_store_export": ([P, P, I64, I64, P, ctypes.c_int, P, P, P, Ptr7, P], ctypes.c_int),
+    "kwb_store_extract": ([P, P, I64, I64, P, I64, P, P, P, Ptr7, P, P, P], ctypes.c_int),
+    "kwb_store_load_counted": ([P, P, P, I64, P, P, P, Ptr7, P, P], ctypes.c_int),
     "kwb_store_repack": ([P, P, P, P], ctypes.c_int),
     "kwb_init_khi": ([P, P, P, P], ctypes.c_int),
 }

@@ -66,8 +66,11 @@ __global__ void shift_kernel(StoreT<F> out, ExchT<F> ex, Geo g, int32_t *__restr
 
 // ---- store load / export / repack ---------------------------------------
 
+// n_dev != NULL: the record count is read on the device (min(*n_dev, n)),
+// so a received message can be appended without a host round trip.
 template <typename F>
-__global__ void load_kernel(Geo g, StoreT<F> st, int64_t n, const int32_t *__restrict__ cx,
+__global__ void load_kernel(Geo g, StoreT<F> st, int64_t n, const int64_t *__restrict__ n_dev,
+                            const int32_t *__restrict__ cx,
                             const int32_t *__restrict__ cy, const int32_t *__restrict__ cz,
                             const F *__restrict__ ox, const F *__restrict__ oy,
                             const F *__restrict__ oz, const F *__restrict__ ux,
@@ -75,6 +78,7 @@ __global__ void load_kernel(Geo g, StoreT<F> st, int64_t n, const int32_t *__res
                             const F *__restrict__ w, int32_t *__restrict__ status) {
     const int V = g.scx * g.scy * g.scz, K = st.frames;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (n_dev) n = min(n, *n_dev);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
         const int x = cx[i], y = cy[i], z = cz[i];
         if (x < 0 || x >= g.nx || y < 0 || y >= g.ny || z < 0 || z >= g.nz) {
@@ -101,8 +105,16 @@ template <typename F>
 __global__ void export_kernel(Geo g, StoreT<F> st, int64_t col0, int64_t col1,
                               const int64_t *__restrict__ cell_start, int clear, int32_t *cx,
                               int32_t *cy, int32_t *cz, F *ox, F *oy, F *oz, F *ux, F *uy, F *uz,
-                              F *w) {
+                              F *w, int64_t capacity, int64_t *count_out, int32_t *status) {
     const int V = g.scx * g.scy * g.scz, K = st.frames;
+    if (capacity >= 0) {   // bounded: all or nothing for the whole column range
+        const int64_t total = cell_start[col1 - col0];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            *count_out = total <= capacity ? total : 0;
+            if (total > capacity) atomicAdd(&status[KWB_ST_GUARD_OVERFLOW], (int)(total - capacity));
+        }
+        if (total > capacity) return;
+    }
     for (int64_t colx = col0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; colx < col1;
          colx += (int64_t)gridDim.x * blockDim.x) {
         const int s = (int)(colx / V), c = (int)(colx % V);
@@ -410,9 +422,9 @@ extern "C" int kwb_particles_shift(const kwb_grid *g, const kwb_store *out,
     return kwb_check_launch("shift_kernel");
 }
 
-extern "C" int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
-                              const int32_t *cx, const int32_t *cy, const int32_t *cz,
-                              void *const f7[7], int32_t *status, kwb_stream_t stream) {
+static int store_load(const kwb_grid *g, const kwb_store *st, int64_t n, const int64_t *n_dev,
+                      const int32_t *cx, const int32_t *cy, const int32_t *cz,
+                      void *const f7[7], int32_t *status, kwb_stream_t stream) {
     int rc = check_grid(g);
     if (rc) return rc;
     if ((rc = check_store(st, "target"))) return rc;
@@ -420,27 +432,44 @@ extern "C" int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
         kwb_set_error("store_load: NULL argument");
         return KWB_EINVAL;
     }
-    if (n == 0) return KWB_OK;
+    if (n <= 0) return KWB_OK;
     Geo geo = geo_of(*g);
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t need = (n + 255) / 256, cap = (int64_t)sm_count() * 16;
     const int blocks = (int)(need < cap ? need : cap);
     if (g->dtype == KWB_F32) {
         const float *const *f = (const float *const *)f7;
-        load_kernel<float><<<blocks, 256, 0, s>>>(geo, store_of<float>(*st), n, cx, cy, cz,
+        load_kernel<float><<<blocks, 256, 0, s>>>(geo, store_of<float>(*st), n, n_dev, cx, cy, cz,
                                                   f[0], f[1], f[2], f[3], f[4], f[5], f[6], status);
     } else {
         const double *const *f = (const double *const *)f7;
-        load_kernel<double><<<blocks, 256, 0, s>>>(geo, store_of<double>(*st), n, cx, cy, cz,
+        load_kernel<double><<<blocks, 256, 0, s>>>(geo, store_of<double>(*st), n, n_dev, cx, cy, cz,
                                                    f[0], f[1], f[2], f[3], f[4], f[5], f[6], status);
     }
     return kwb_check_launch("load_kernel");
 }
 
-extern "C" int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin,
-                                int64_t col_end, const int64_t *cell_start, int clear,
-                                int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
-                                kwb_stream_t stream) {
+extern "C" int kwb_store_load(const kwb_grid *g, const kwb_store *st, int64_t n,
+                              const int32_t *cx, const int32_t *cy, const int32_t *cz,
+                              void *const f7[7], int32_t *status, kwb_stream_t stream) {
+    return store_load(g, st, n, nullptr, cx, cy, cz, f7, status, stream);
+}
+
+extern "C" int kwb_store_load_counted(const kwb_grid *g, const kwb_store *st, const int64_t *n_dev,
+                                      int64_t capacity, const int32_t *cx, const int32_t *cy,
+                                      const int32_t *cz, void *const f7[7], int32_t *status,
+                                      kwb_stream_t stream) {
+    if (!n_dev) {
+        kwb_set_error("store_load_counted: NULL count");
+        return KWB_EINVAL;
+    }
+    return store_load(g, st, capacity, n_dev, cx, cy, cz, f7, status, stream);
+}
+
+static int store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin,
+                        int64_t col_end, const int64_t *cell_start, int clear, int32_t *cx,
+                        int32_t *cy, int32_t *cz, void *const f7[7], int64_t capacity,
+                        int64_t *count_out, int32_t *status, kwb_stream_t stream) {
     int rc = check_grid(g);
     if (rc) return rc;
     if ((rc = check_store(st, "source"))) return rc;
@@ -450,27 +479,54 @@ extern "C" int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t 
                       (long long)col_begin, (long long)col_end, (long long)ncol);
         return KWB_EINVAL;
     }
-    if (!cell_start || !cx || !cy || !cz || !f7) {
+    if (!cell_start || !cx || !cy || !cz || !f7 ||
+        (capacity >= 0 && (!count_out || !status))) {
         kwb_set_error("store_export: NULL argument");
         return KWB_EINVAL;
     }
-    if (col_begin == col_end) return KWB_OK;
-    Geo geo = geo_of(*g);
     cudaStream_t s = (cudaStream_t)stream;
+    if (col_begin == col_end) {
+        if (capacity >= 0) return cudaMemsetAsync(count_out, 0, sizeof(int64_t), s) == cudaSuccess
+                                      ? KWB_OK : kwb_check_launch("store_export memset");
+        return KWB_OK;
+    }
+    Geo geo = geo_of(*g);
     const int64_t need = (col_end - col_begin + 255) / 256, cap = (int64_t)sm_count() * 16;
     const int blocks = (int)(need < cap ? need : cap);
     if (g->dtype == KWB_F32) {
         float *const *f = (float *const *)f7;
         export_kernel<float><<<blocks, 256, 0, s>>>(geo, store_of<float>(*st), col_begin, col_end,
                                                     cell_start, clear, cx, cy, cz, f[0], f[1], f[2],
-                                                    f[3], f[4], f[5], f[6]);
+                                                    f[3], f[4], f[5], f[6], capacity, count_out,
+                                                    status);
     } else {
         double *const *f = (double *const *)f7;
         export_kernel<double><<<blocks, 256, 0, s>>>(geo, store_of<double>(*st), col_begin, col_end,
                                                      cell_start, clear, cx, cy, cz, f[0], f[1], f[2],
-                                                     f[3], f[4], f[5], f[6]);
+                                                     f[3], f[4], f[5], f[6], capacity, count_out,
+                                                     status);
     }
     return kwb_check_launch("export_kernel");
+}
+
+extern "C" int kwb_store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begin,
+                                int64_t col_end, const int64_t *cell_start, int clear,
+                                int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
+                                kwb_stream_t stream) {
+    return store_export(g, st, col_begin, col_end, cell_start, clear, cx, cy, cz, f7, -1, nullptr,
+                        nullptr, stream);
+}
+
+extern "C" int kwb_store_extract(const kwb_grid *g, const kwb_store *st, int64_t col_begin,
+                                 int64_t col_end, const int64_t *cell_start, int64_t capacity,
+                                 int32_t *cx, int32_t *cy, int32_t *cz, void *const f7[7],
+                                 int64_t *count_out, int32_t *status, kwb_stream_t stream) {
+    if (capacity < 0) {
+        kwb_set_error("store_extract: negative capacity");
+        return KWB_EINVAL;
+    }
+    return store_export(g, st, col_begin, col_end, cell_start, 1, cx, cy, cz, f7, capacity,
+                        count_out, status, stream);
 }
 
 extern "C" int kwb_store_repack(const kwb_grid *g, const kwb_store *src, const kwb_store *dst,

@@ -36,6 +36,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .. import _lib
+from ..errors import AllocationError
 from .params import SimParams
 
 E3 = ("Ex", "Ey", "Ez")
@@ -182,6 +184,8 @@ class DecomposedSimulation:
         self.locals = {r: local_factory(local_params(params, lay))
                        for r, lay in self.layouts.items()}
         self.step_count = 0
+        self._xbuf = {}       # (rank, direction) -> fixed-capacity guard-exchange buffers
+        self._xcap = None     # records per species per message
 
     # -- state in / out --------------------------------------------------------
     def load_global(self, fields=None, particles=None):
@@ -256,12 +260,17 @@ class DecomposedSimulation:
         return pk
 
     # -- the cycle -----------------------------------------------------------------
-    def step(self):
+    def step(self, checked: bool = True):
+        """One PIC cycle on every slab.  checked=True (the reference's
+        synchronous semantics): a guard-exchange capacity overflow is
+        detected right away (one flag all-reduced per step) and the exchange
+        redone with larger messages.  checked=False (enqueue_step): no host
+        synchronisation at all; an overflow surfaces in check_status()."""
         for sim in self.locals.values():
             sim._drain_status(keep=1)
             sim.advance_particles()
         self._exchange_j()
-        self._exchange_particles()
+        self._exchange_particles(checked)
         for sim in self.locals.values():
             sim.faraday_half()
             sim.ampere()
@@ -273,6 +282,9 @@ class DecomposedSimulation:
             sim.step_count += 1
             sim._post_status()
         self.step_count += 1
+
+    def enqueue_step(self):
+        self.step(checked=False)
 
     def run(self, steps):
         for _ in range(steps):
@@ -356,52 +368,155 @@ class DecomposedSimulation:
                 J[c][nzl:nzl + gp] += fu[c]
                 J[c][gp:2 * gp] += fl[c]
 
-    def _exchange_particles(self):
+    def _exchange_particles(self, checked=True):
+        stores = [st for sim in self.locals.values() for st in sim.stores]
+        if stores and all(hasattr(st, "extract_into") for st in stores):
+            return self._exchange_particles_device(checked)
+        return self._exchange_particles_sized()
+
+    def _guard_cap(self):
+        """Records per species per message: 1/8 of a guard layer's mean
+        particle load (a thermal plasma sends ~0.5 %, v dt = 0.55 cells ~7 %),
+        at least 4096."""
+        if self._xcap is None:
+            est = 0
+            for r, lay in self.layouts.items():
+                for st in self.locals[r].stores:
+                    cols = st.n_super_cells * st.capacity
+                    per_guard = st.sc_grid.x * st.sc_grid.y * st.capacity * lay.ghost_layers
+                    est = max(est, int(st.census() / max(cols, 1) * per_guard))
+            self._xcap = max(4096, est // 8)
+        return self._xcap
+
+    def _exchange_particles_device(self, checked):
+        """Guard-layer particles to the neighbour that owns them, with no host
+        synchronisation: per rank and direction one fixed-capacity (3, S*cap)
+        int32 and (7, S*cap) float message (species i in columns [i*cap,
+        (i+1)*cap)) plus an S-vector of counts, all filled and consumed on
+        the device (kwb_store_extract / kwb_store_load_counted).  A range
+        with more than cap records is not extracted and raises the
+        guard-overflow status word; checked=True all-reduces that flag and
+        redoes the exchange with doubled messages."""
+        for _attempt in range(8):
+            cap = self._guard_cap()
+            n_sp = len(self.params.species)
+            flags = []
+            sends, recvs, incoming = [], [], []
+            for r, lay in self.layouts.items():
+                sim = self.locals[r]
+                dev, tdt = sim.device, sim.stores[0].tdtype
+                (b0, b1), (t0, t1) = lay.guard_layers()
+                for direction, (l0, l1), shift, peer in ((DOWN, (b0, b1), lay.nzl, lay.lower),
+                                                         (UP, (t0, t1), -lay.nzl, lay.upper)):
+                    key = (r, direction)
+                    buf = self._xbuf.get(key)
+                    if buf is None or buf[0].shape[1] != n_sp * cap:
+                        buf = tuple(torch.empty(shape, dtype=dt, device=dev) for shape, dt in (
+                            ((3, n_sp * cap), torch.int32), ((7, n_sp * cap), tdt),
+                            ((n_sp,), torch.int64), ((3, n_sp * cap), torch.int32),
+                            ((7, n_sp * cap), tdt), ((n_sp,), torch.int64)))
+                        self._xbuf[key] = buf
+                    s_int, s_flt, s_cnt, r_int, r_flt, r_cnt = buf
+                    for i, st in enumerate(sim.stores):
+                        per_layer = st.sc_grid.x * st.sc_grid.y * st.capacity
+                        cols = (l0 * per_layer, l1 * per_layer)
+                        st.extract_into(cols, st.column_starts(cols), s_int, s_flt, s_cnt[i:i + 1],
+                                        sim._status[i], cap, offset=i * cap)
+                    s_int[2] += shift
+                    sends += [(r, peer, TAG_PCNT + direction, s_cnt),
+                              (r, peer, TAG_PINT + direction, s_int),
+                              (r, peer, TAG_PFLT + direction, s_flt)]
+                    src = lay.upper if direction == DOWN else lay.lower
+                    recvs += [(src, r, TAG_PCNT + direction, r_cnt),
+                              (src, r, TAG_PINT + direction, r_int),
+                              (src, r, TAG_PFLT + direction, r_flt)]
+                    incoming.append((sim, r_int, r_flt, r_cnt))
+                flags.append(sim._status[:, _lib.ST_GUARD_OVERFLOW].sum())
+            self.transport.exchange(sends, recvs)
+            for sim, r_int, r_flt, r_cnt in incoming:
+                for i, st in enumerate(sim.stores):
+                    st.append_counted(r_int, r_flt, r_cnt[i], cap, sim._status[i], offset=i * cap)
+            if not checked:
+                return
+            over = torch.stack(flags).sum().to(torch.float64).reshape(1)
+            if isinstance(self.transport, DistTransport):
+                self.transport.dist.all_reduce(over)
+            if float(over.item()) == 0:
+                return
+            # nothing of an overflowing range left its guard layer: clear the
+            # flag, double the messages, exchange again (emptied ranges send 0)
+            for sim in self.locals.values():
+                sim._status[:, _lib.ST_GUARD_OVERFLOW] = 0
+            self._xcap = 2 * cap
+        raise AllocationError("guard-layer particle exchange keeps overflowing")
+
+    def _exchange_particles_sized(self):
+        """Guard-layer particles to the neighbour that owns them, messages
+        sized on the host (used with stores that have no device extract,
+        e.g. the CPU oracle in the gloo tests).  Per rank and direction ONE
+        (3, n) int32 and ONE (7, n) float message carry every species (plus
+        an n_species count vector)."""
         n_sp = len(self.params.species)
-        out = {}
-        cnt_sends, cnt_recvs = [], []
+        plans = []   # (rank, direction, peer, shift, [(store, cols, start)])
         for r, lay in self.layouts.items():
             sim = self.locals[r]
             (b0, b1), (t0, t1) = lay.guard_layers()
-            for i, st in enumerate(sim.stores):
-                per_layer = st.sc_grid.x * st.sc_grid.y * st.capacity
-                for direction, (l0, l1), shift, peer in ((DOWN, (b0, b1), lay.nzl, lay.lower),
-                                                         (UP, (t0, t1), -lay.nzl, lay.upper)):
-                    rec = st.packed_device(columns=(l0 * per_layer, l1 * per_layer), clear=True)
-                    rec["cz"] = rec["cz"] + shift
-                    ints = torch.stack([rec["cx"], rec["cy"], rec["cz"]])
-                    flts = torch.stack([rec[c] for c in ("ox", "oy", "oz", "ux", "uy", "uz", "w")])
-                    tag = 2 * i + direction
-                    out[(r, peer, tag)] = (ints, flts)
-                    cnt_sends.append((r, peer, TAG_PCNT + tag,
-                                      torch.tensor([ints.shape[1]], dtype=torch.int64,
-                                                   device=sim.device)))
-            for i in range(n_sp):
-                for direction, peer in ((DOWN, lay.upper), (UP, lay.lower)):
-                    cnt_recvs.append((peer, r, TAG_PCNT + 2 * i + direction,
-                                      torch.zeros(1, dtype=torch.int64, device=sim.device)))
-        self.transport.exchange(cnt_sends, cnt_recvs)
-        sends, recvs, incoming = [], [], []
-        for (r, peer, tag), (ints, flts) in out.items():
-            sends += [(r, peer, TAG_PINT + tag, ints), (r, peer, TAG_PFLT + tag, flts)]
-        for src, r, tag, cnt in cnt_recvs:
-            n = int(cnt.item())
+            for direction, (l0, l1), shift, peer in ((DOWN, (b0, b1), lay.nzl, lay.lower),
+                                                     (UP, (t0, t1), -lay.nzl, lay.upper)):
+                per = []
+                for st in sim.stores:
+                    per_layer = st.sc_grid.x * st.sc_grid.y * st.capacity
+                    cols = (l0 * per_layer, l1 * per_layer)
+                    per.append((st, cols, st.column_starts(cols)))
+                plans.append((r, direction, peer, shift, per))
+        if not plans:
+            return
+        counts = torch.stack([start[-1] for *_, per in plans for _, _, start in per]).cpu()
+        sends, cnt_sends, k = [], [], 0
+        for r, direction, peer, shift, per in plans:
             sim = self.locals[r]
-            i = (tag - TAG_PCNT) // 2
+            ns = [int(counts[k + i]) for i in range(n_sp)]
+            k += n_sp
+            n = sum(ns)
+            ints = torch.empty((3, max(n, 1)), dtype=torch.int32, device=sim.device)
+            flts = torch.empty((7, max(n, 1)), dtype=sim.stores[0].tdtype, device=sim.device)
+            o = 0
+            for (st, cols, start), m in zip(per, ns):
+                st.export_into(cols, start, ints, flts, offset=o, clear=True)
+                o += m
+            ints, flts = ints[:, :n], flts[:, :n]
+            if n:
+                ints[2] += shift
+            cnt_sends.append((r, peer, TAG_PCNT + direction,
+                              torch.tensor(ns, dtype=torch.int64, device=sim.device)))
+            sends += [(r, peer, TAG_PINT + direction, ints), (r, peer, TAG_PFLT + direction, flts)]
+        cnt_recvs = []
+        for r, lay in self.layouts.items():
+            sim = self.locals[r]
+            for direction, peer in ((DOWN, lay.upper), (UP, lay.lower)):
+                cnt_recvs.append((peer, r, TAG_PCNT + direction,
+                                  torch.zeros(n_sp, dtype=torch.int64, device=sim.device)))
+        self.transport.exchange(cnt_sends, cnt_recvs)
+        rcounts = torch.stack([c for *_, c in cnt_recvs]).cpu()
+        recvs, incoming = [], []
+        for (src, r, tag, _), ns in zip(cnt_recvs, rcounts.tolist()):
+            sim = self.locals[r]
+            n = sum(ns)
             ints = torch.empty((3, n), dtype=torch.int32, device=sim.device)
-            flts = torch.empty((7, n), dtype=sim.stores[i].tdtype, device=sim.device)
-            recvs += [(src, r, TAG_PINT + tag - TAG_PCNT, ints),
-                      (src, r, TAG_PFLT + tag - TAG_PCNT, flts)]
-            incoming.append((r, i, ints, flts))
+            flts = torch.empty((7, n), dtype=sim.stores[0].tdtype, device=sim.device)
+            direction = tag - TAG_PCNT
+            recvs += [(src, r, TAG_PINT + direction, ints), (src, r, TAG_PFLT + direction, flts)]
+            incoming.append((r, ns, ints, flts))
         self.transport.exchange(sends, recvs)
-        for r, i, ints, flts in incoming:
-            if ints.shape[1] == 0:
-                continue
-            st = self.locals[r].stores[i]
-            rec = {"cx": ints[0], "cy": ints[1], "cz": ints[2]}
-            for k, c in enumerate(("ox", "oy", "oz", "ux", "uy", "uz", "w")):
-                rec[c] = flts[k]
-            st.append(rec, status=self.locals[r]._status[i])
+        for r, ns, ints, flts in incoming:
+            o = 0
+            for i, m in enumerate(ns):
+                if m:
+                    rec = {"cx": ints[0, o:o + m], "cy": ints[1, o:o + m], "cz": ints[2, o:o + m]}
+                    for kk, c in enumerate(("ox", "oy", "oz", "ux", "uy", "uz", "w")):
+                        rec[c] = flts[kk, o:o + m]
+                    self.locals[r].stores[i].append(rec, status=self.locals[r]._status[i])
+                o += m
 
     def _exchange_e_top(self):
         sends, recvs, sets = [], [], []

@@ -252,6 +252,58 @@ class SuperCellStore:
                       _stream(stream, self.device))
         return {k: v[:n] for k, v in out.items()}
 
+    def column_starts(self, columns):
+        """Exclusive prefix sum (device, int64, length n+1) of the particle
+        counts of the column range `columns` = (begin, end)."""
+        c0, c1 = columns
+        cnt = (self.current.front[c0:c1] + self.current.back[c0:c1]).to(torch.int64)
+        start = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(cnt, 0, out=start[1:])
+        return start
+
+    def export_into(self, columns, start, ints, flts, offset=0, clear=False, stream=None):
+        """kwb_store_export of the column range into rows of caller buffers:
+        ints (3, m) int32 (cx, cy, cz) and flts (7, m) storage-type
+        (ox oy oz ux uy uz w), records placed from column `offset`; `start`
+        from column_starts().  No host synchronisation."""
+        c0, c1 = columns
+        g = self._grid_struct()
+        isz, fsz = ints.element_size(), flts.element_size()
+        ip = [ints.data_ptr() + (k * ints.stride(0) + offset) * isz for k in range(3)]
+        fp = [flts.data_ptr() + (k * flts.stride(0) + offset) * fsz for k in range(7)]
+        _lib.call("kwb_store_export", _lib.ctypes.byref(g),
+                  _lib.ctypes.byref(self.current.cstruct()), c0, c1, start.data_ptr(),
+                  int(bool(clear)), ip[0], ip[1], ip[2],
+                  _lib.Ptr7(*fp), _stream(stream, self.device))
+
+    def extract_into(self, columns, start, ints, flts, count_out, status, capacity,
+                     offset=0, stream=None):
+        """kwb_store_extract: move the particles of the column range into rows
+        of caller buffers (from column `offset`, at most `capacity` records,
+        all or nothing); the count lands in count_out (device int64)."""
+        c0, c1 = columns
+        g = self._grid_struct()
+        isz, fsz = ints.element_size(), flts.element_size()
+        ip = [ints.data_ptr() + (k * ints.stride(0) + offset) * isz for k in range(3)]
+        fp = [flts.data_ptr() + (k * flts.stride(0) + offset) * fsz for k in range(7)]
+        _lib.call("kwb_store_extract", _lib.ctypes.byref(g),
+                  _lib.ctypes.byref(self.current.cstruct()), c0, c1, start.data_ptr(), capacity,
+                  ip[0], ip[1], ip[2], _lib.Ptr7(*fp), count_out.data_ptr(), status.data_ptr(),
+                  _stream(stream, self.device))
+
+    def append_counted(self, ints, flts, count, capacity, status, offset=0, stream=None):
+        """kwb_store_load_counted: append min(count, capacity) records held in
+        rows of (3, m) int32 / (7, m) buffers from column `offset`; `count` is
+        a device int64 (no host synchronisation)."""
+        g = self._grid_struct()
+        isz, fsz = ints.element_size(), flts.element_size()
+        ip = [ints.data_ptr() + (k * ints.stride(0) + offset) * isz for k in range(3)]
+        fp = [flts.data_ptr() + (k * flts.stride(0) + offset) * fsz for k in range(7)]
+        _lib.call("kwb_store_load_counted", _lib.ctypes.byref(g),
+                  _lib.ctypes.byref(self.current.cstruct()), count.data_ptr(), capacity,
+                  ip[0], ip[1], ip[2], _lib.Ptr7(*fp), status.data_ptr(),
+                  _stream(stream, self.device))
+
     def append(self, arrays: dict, stream=None, status=None) -> None:
         """Append particle records (device tensors or host arrays; global
         cells in this store's grid) to their columns without resizing.

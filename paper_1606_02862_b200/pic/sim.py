@@ -333,6 +333,11 @@ class Simulation:
             raise AllocationError(
                 f"{lost} particle(s) did not fit their cell column or the exchange buffer "
                 "(enqueue_step has no redo; use step())")
+        guard = int(st[:, _lib.ST_GUARD_OVERFLOW].sum())
+        if guard:
+            raise AllocationError(
+                f"{guard} guard-layer particle(s) exceeded the z-slab exchange message "
+                "capacity (DecomposedSimulation.enqueue_step has no redo; use step())")
         for i, store in enumerate(self.stores):
             store.reserve(int(st[i, _lib.ST_MAX_COUNT]))
 

@@ -64,6 +64,22 @@ class _Store:
             out[k] = torch.from_numpy(np.asarray(v, dtype=dt))
         return out
 
+    def column_starts(self, columns):
+        """Only the total ([-1]) is used by the decomposition."""
+        V = self.capacity
+        st = self.st
+        n = sum(int(st.occ[f].sum()) for sc in range(columns[0] // V, columns[1] // V)
+                for f in st.frames_of(sc))
+        return torch.tensor([0, n], dtype=torch.int64)
+
+    def export_into(self, columns, start, ints, flts, offset=0, clear=False):
+        rec = self.packed_device(columns, clear)
+        n = rec["cx"].shape[0]
+        for k, c in enumerate(("cx", "cy", "cz")):
+            ints[k, offset:offset + n] = rec[c]
+        for k, c in enumerate(COLS):
+            flts[k, offset:offset + n] = rec[c]
+
     def append(self, rec, status=None):
         st = self.st
         n = rec["cx"].shape[0]

@@ -78,3 +78,46 @@ def test_decomposed_diagnostics_match_single_domain():
     assert a["kinetic_energy"] == pytest.approx(b["kinetic_energy"], rel=1e-12)
     assert a["field_energy"] == pytest.approx(b["field_energy"], rel=1e-9)
     assert a["max_div_b"] <= 1e-12 and b["max_div_b"] <= 1e-12
+
+
+def _fast_pair(world):
+    from paper_1606_02862_b200.pic import SimParams, default_species, init_khi
+    from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
+    p = SimParams(cells=(16, 16, 24), species=default_species(4, 4.0), particles_per_cell=4,
+                  dtype=np.float64, stream_velocity=0.0, perturbation=0.0, thermal_u=1.0)
+    ref = init_khi(p, seed=5, validate=False)
+    dec = DecomposedSimulation(p, world, range(world), LoopbackTransport())
+    dec.load_global(particles=[st.packed() for st in ref.stores])
+    dec.refresh_guards()
+    return p, ref, dec
+
+
+def test_guard_exchange_overflow_is_redone():
+    """Fixed-capacity guard messages far too small for a hot plasma: the
+    checked step detects the overflow, doubles the messages and redoes the
+    exchange -- the result equals the single-domain run, nothing is lost."""
+    p, ref, dec = _fast_pair(2)
+    dec._xcap = 2
+    n0 = ref.census()
+    for _ in range(2):
+        ref.step()
+        dec.step()
+        dec.check_status()
+        assert dec.census() == n0
+    assert dec._xcap > 2
+    for i in range(len(p.species)):
+        mine = _sorted({k: np.concatenate([dec.owned_particles(r, i)[k] for r in range(2)])
+                        for k in PK})
+        want = _sorted(ref.stores[i].packed())
+        for k in ("cx", "cy", "cz"):
+            np.testing.assert_array_equal(mine[k], want[k])
+
+
+def test_guard_exchange_overflow_raises_when_unchecked():
+    from paper_1606_02862_b200.errors import AllocationError
+    p, ref, dec = _fast_pair(2)
+    dec._xcap = 2
+    with pytest.raises(AllocationError, match="guard-layer"):
+        for _ in range(3):
+            dec.enqueue_step()
+        dec.check_status()
