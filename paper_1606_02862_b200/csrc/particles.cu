@@ -543,6 +543,88 @@ extern "C" int kwb_store_repack(const kwb_grid *g, const kwb_store *src, const k
     return kwb_check_launch("repack_kernel");
 }
 
+// CIC/TSC charge density with the current deposit's strategy: a thread owns
+// a cell, so every particle it reads deposits into the same 3x3x3 stencil
+// around that cell -- 27 float64 register accumulators, reduced into a
+// shared (scx+2)(scy+2)(scz+2) tile in 27 barrier-separated conflict-free
+// sweeps, the tile flushed with one global red.add per entry.  Same terms
+// as rho_kernel (pic/kernels.py:291-326), summed in a different order
+// (float64; the validation compares rho within tolerance).  The per-particle
+// atomic version costs ~27 random float64 atomics per particle.
+template <typename F, int ORDER>
+__global__ void __launch_bounds__(256) rho_reg_kernel(Geo g, StoreT<F> st, double q_inv_vol,
+                                                      double *__restrict__ rho) {
+    static_assert(ORDER == 1 || ORDER == 2, "3-point stencils only");
+    constexpr int H = Shape<ORDER>::H;
+    __shared__ double tile[(16 + 2) * (16 + 2) * (16 + 2)];
+    const int V = g.scx * g.scy * g.scz;
+    const int tx = g.scx + 2, ty = g.scy + 2, tz = g.scz + 2, T = tx * ty * tz;
+    const int s = blockIdx.x, c = threadIdx.x;
+    const bool owner = c < V;
+    const int bx = s % g.gx, by = (s / g.gx) % g.gy, bz = s / (g.gx * g.gy);
+    const int lx = c % g.scx, ly = (c / g.scx) % g.scy, lz = c / (g.scx * g.scy);
+    for (int i = c; i < T; i += blockDim.x) tile[i] = 0.0;
+    double acc[3][3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) acc[a][b][d] = 0.0;
+    if (owner) {
+        for_column(st, s, c, V, [&](int64_t q) {
+            const double qw = q_inv_vol * (double)st.w[q];
+            double wx[3], wy[3], wz[3];
+            if (ORDER == 2) {
+                double o, l, r;
+                o = (double)st.ox[q] - 0.5; l = 0.5 * ((0.5 - o) * (0.5 - o)); r = 0.5 * ((0.5 + o) * (0.5 + o));
+                wx[0] = l; wx[1] = (1.0 - l) - r; wx[2] = r;
+                o = (double)st.oy[q] - 0.5; l = 0.5 * ((0.5 - o) * (0.5 - o)); r = 0.5 * ((0.5 + o) * (0.5 + o));
+                wy[0] = l; wy[1] = (1.0 - l) - r; wy[2] = r;
+                o = (double)st.oz[q] - 0.5; l = 0.5 * ((0.5 - o) * (0.5 - o)); r = 0.5 * ((0.5 + o) * (0.5 + o));
+                wz[0] = l; wz[1] = (1.0 - l) - r; wz[2] = r;
+            } else {
+                constexpr int NP = Shape<ORDER>::NP;
+                F sx[NP], sy[NP], sz[NP];
+                shape_into<F, ORDER>((double)st.ox[q], sx);
+                shape_into<F, ORDER>((double)st.oy[q], sy);
+                shape_into<F, ORDER>((double)st.oz[q], sz);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {   // CIC support: indices H-1 .. H+1
+                    wx[a] = (double)sx[H - 1 + a];
+                    wy[a] = (double)sy[H - 1 + a];
+                    wz[a] = (double)sz[H - 1 + a];
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) acc[a][b][d] += ((qw * wx[a]) * wy[b]) * wz[d];
+        });
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                if (owner) tile[((lz + d) * ty + (ly + b)) * tx + (lx + a)] += acc[a][b][d];
+                __syncthreads();
+            }
+    const int ox = bx * g.scx - 1, oy = by * g.scy - 1, oz = bz * g.scz - 1;
+    for (int i = c; i < T; i += blockDim.x) {
+        const double v = tile[i];
+        if (v != 0.0) {
+            const int a = i % tx, b = (i / tx) % ty, d = i / (tx * ty);
+            atomicAdd(rho + fidx(pymod(ox + a, g.nx), pymod(oy + b, g.ny), pymod(oz + d, g.nz),
+                                 g.nx, g.ny), v);
+        }
+    }
+}
+
 extern "C" int kwb_charge_density(const kwb_grid *g, const kwb_species *sp, const kwb_store *st,
                                   int shape_order, double *rho, kwb_stream_t stream) {
     int rc = check_grid(g);
@@ -555,19 +637,23 @@ extern "C" int kwb_charge_density(const kwb_grid *g, const kwb_species *sp, cons
     Geo geo = geo_of(*g);
     cudaStream_t s = (cudaStream_t)stream;
     const int n_sc = g->gx * g->gy * g->gz, th = block_threads(g);
+    // register/tile kernel for CIC/TSC when the super cell fits its static tile
+    const bool reg = g->scx <= 16 && g->scy <= 16 && g->scz <= 16;
 #define KWB_RHO(T, O) rho_kernel<T, O><<<n_sc, th, 0, s>>>(geo, store_of<T>(*st), sp->q_inv_vol, rho)
+#define KWB_RHOR(T, O) rho_reg_kernel<T, O><<<n_sc, th, 0, s>>>(geo, store_of<T>(*st), sp->q_inv_vol, rho)
     if (g->dtype == KWB_F32) {
-        if (shape_order == 1) KWB_RHO(float, 1);
-        else if (shape_order == 2) KWB_RHO(float, 2);
+        if (shape_order == 1) { if (reg) KWB_RHOR(float, 1); else KWB_RHO(float, 1); }
+        else if (shape_order == 2) { if (reg) KWB_RHOR(float, 2); else KWB_RHO(float, 2); }
         else if (shape_order == 3) KWB_RHO(float, 3);
         else { kwb_set_error("bad shape_order %d", shape_order); return KWB_EINVAL; }
     } else {
-        if (shape_order == 1) KWB_RHO(double, 1);
-        else if (shape_order == 2) KWB_RHO(double, 2);
+        if (shape_order == 1) { if (reg) KWB_RHOR(double, 1); else KWB_RHO(double, 1); }
+        else if (shape_order == 2) { if (reg) KWB_RHOR(double, 2); else KWB_RHO(double, 2); }
         else if (shape_order == 3) KWB_RHO(double, 3);
         else { kwb_set_error("bad shape_order %d", shape_order); return KWB_EINVAL; }
     }
 #undef KWB_RHO
+#undef KWB_RHOR
     return kwb_check_launch("rho_kernel");
 }
 
