@@ -599,6 +599,80 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
     }
 }
 
+// float64 storage: the same register deposit in double (108 registers of
+// accumulators, so these kernels run one CTA per SM); J in float64 is
+// compared at 1e-13 and the FMA-contracted sums stay far inside it.
+struct RegAccD {
+    double a[3][2][3][3];  // [component][ja-1][j1-1][j2-1]
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a_ = 0; a_ < 2; ++a_)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) a[c][a_][b][d] = 0.0;
+    }
+    __device__ __forceinline__ double get(int c, int a_, int b, int d) const {
+        return a[c][a_][b][d];
+    }
+};
+
+template <int ORDER>
+__device__ __forceinline__ void shape123d(double x, double (&s)[3]) {
+    if (ORDER == 2) {
+        const double a = 1.0 - x, b = x - 0.5;
+        s[0] = 0.5 * (a * a);
+        s[1] = __fma_rn(-b, b, 0.75);
+        s[2] = 0.5 * (x * x);
+    } else {
+        s[0] = fmax(0.5 - x, 0.0);
+        s[1] = 1.0 - fabs(x - 0.5);
+        s[2] = fmax(x - 0.5, 0.0);
+    }
+}
+
+template <int ORDER>
+__device__ __forceinline__ void deposit_stay_d(RegAccD &R, double oox, double ooy, double ooz,
+                                               double nox, double noy, double noz, double fwx,
+                                               double fwy, double fwz) {
+    double s0[3][3], ds[3][3];
+    {
+        double s1[3];
+        shape123d<ORDER>(oox, s0[0]);
+        shape123d<ORDER>(nox, s1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ds[0][i] = s1[i] - s0[0][i];
+        shape123d<ORDER>(ooy, s0[1]);
+        shape123d<ORDER>(noy, s1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ds[1][i] = s1[i] - s0[1][i];
+        shape123d<ORDER>(ooz, s0[2]);
+        shape123d<ORDER>(noz, s1);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ds[2][i] = s1[i] - s0[2][i];
+    }
+    const double fw[3] = {fwx, fwy, fwz};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
+        const double p1 = fw[c] * ds[c][0];
+        const double p2 = fw[c] * (ds[c][0] + ds[c][1]);
+#pragma unroll
+        for (int j1 = 0; j1 < 3; ++j1) {
+            const double u = __fma_rn(0.5, ds[a1][j1], s0[a1][j1]);
+            const double v = __fma_rn(1.0 / 3.0, ds[a1][j1], 0.5 * s0[a1][j1]);
+#pragma unroll
+            for (int j2 = 0; j2 < 3; ++j2) {
+                const double T = __fma_rn(u, s0[a2][j2], v * ds[a2][j2]);
+                R.a[c][0][j1][j2] = __fma_rn(p1, T, R.a[c][0][j1][j2]);
+                R.a[c][1][j1][j2] = __fma_rn(p2, T, R.a[c][1][j1][j2]);
+            }
+        }
+    }
+}
+
 // Tile offset of accumulator (c, ja, j1, j2) relative to the owner cell.
 __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int jx, int jy) {
     int ox, oy, oz;
@@ -613,7 +687,7 @@ template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
 #ifndef KWB_MIN_BLOCKS
 #define KWB_MIN_BLOCKS 2
 #endif
-__global__ void __launch_bounds__(kMaxCells, KWB_MIN_BLOCKS)
+__global__ void __launch_bounds__(kMaxCells, sizeof(F) == 4 ? KWB_MIN_BLOCKS : 1)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
                int32_t *__restrict__ status) {
     constexpr int H = Shape<ORDER>::H;
@@ -698,7 +772,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     for (int o = 16; o > 0; o >>= 1) n_w = max(n_w, __shfl_xor_sync(0xffffffffu, n_w, o));
     __syncthreads();
 
-    RegAcc R;
+    std::conditional_t<sizeof(F) == 4, RegAcc, RegAccD> R;
     if (REGACC) R.zero();
     const double qm = sp.qm_half_dt;
     const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
@@ -896,9 +970,14 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #endif
             else if (REGACC && dcx == 0 && dcy == 0 && dcz == 0) {
                 const double ww = (double)w;
-                deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox, (float)noy,
-                                    (float)noz, (float)(sp.fac[0] * ww), (float)(sp.fac[1] * ww),
-                                    (float)(sp.fac[2] * ww));
+                if constexpr (sizeof(F) == 4)
+                    deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox,
+                                        (float)noy, (float)noz, (float)(sp.fac[0] * ww),
+                                        (float)(sp.fac[1] * ww), (float)(sp.fac[2] * ww));
+                else
+                    deposit_stay_d<ORDER>(R, (double)ox, (double)oy, (double)oz, (double)nox,
+                                          (double)noy, (double)noz, sp.fac[0] * ww,
+                                          sp.fac[1] * ww, sp.fac[2] * ww);
             } else {
 #ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
                 queue = true;

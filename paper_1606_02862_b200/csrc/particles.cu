@@ -376,8 +376,8 @@ extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
         }
     } else {
         switch (shape_order) {
-            case 1: return dispatch_advance<double, 1, false>(g, sp, in, out, ex, E, B, J, status, s);
-            case 2: return dispatch_advance<double, 2, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 1: return dispatch_advance<double, 1, true>(g, sp, in, out, ex, E, B, J, status, s);
+            case 2: return dispatch_advance<double, 2, true>(g, sp, in, out, ex, E, B, J, status, s);
             case 3: return dispatch_advance<double, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
         }
     }
