@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -138,6 +139,12 @@ class Simulation:
         self._status_ring = [torch.zeros_like(self._status_host).pin_memory() for _ in range(2)]
         self._pending = []
         self._exchange = None
+        # CUDA graphs of the whole cycle for enqueue_step (validate=False):
+        # one per (current, spare) buffer assignment, re-captured whenever a
+        # buffer is reallocated.  Launch-bound grids (C1: seven launches of
+        # 10-70 us) run as one graph launch.
+        self.use_graphs = os.environ.get("KWB_NO_GRAPHS", "") == ""
+        self._graphs = {}
         self._rho_prev = None
         self._G_prev = None
         self._resid = torch.zeros(2, dtype=torch.float64, device=self.device)
@@ -205,13 +212,46 @@ class Simulation:
         host memory behind an event and inspected two steps later (by then
         the event has long completed, so no stall): columns passing GROW_AT
         grow before they can overflow, and any violation raises at the latest
-        in check_status()."""
+        in check_status().  With validate=False the cycle is replayed from a
+        CUDA graph (captured on first use of each buffer assignment)."""
         self._drain_status(keep=1)
-        self._begin_step()
-        self._enqueue_particles()
-        self._enqueue_fields()
+        if self.use_graphs and not self.validate and self.step_count > 0:
+            self._graph_step()
+        else:
+            self._begin_step()
+            self._enqueue_particles()
+            self._enqueue_fields()
         self.step_count += 1
         self._post_status()
+
+    def _graph_key(self):
+        ex = self._exchange_buffer()
+        key = [ex.count.data_ptr(), ex.capacity, self.fields._buf.data_ptr()]
+        for st in self.stores:
+            st.spare()   # both column buffers exist before a capture
+            key += [st._cols[0].ox.data_ptr(), st._cols[1].ox.data_ptr(), st.frames_per_sc]
+        return tuple(key)
+
+    def _graph_step(self):
+        key = self._graph_key()
+        g = self._graphs.get(key)
+        if g is None:
+            if len(self._graphs) >= 4:   # buffers were reallocated: drop stale graphs
+                self._graphs.clear()
+            cur = torch.cuda.current_stream(self.device)
+            cap = torch.cuda.Stream(self.device)
+            cap.wait_stream(cur)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                self._enqueue_particles()
+                self._enqueue_fields()
+            cur.wait_stream(cap)
+            for st in self.stores:   # the capture only recorded the work: undo its swaps
+                st.swap()
+            self._graphs[key] = g
+        g.replay()
+        for st in self.stores:
+            st.swap()
 
     def _post_status(self):
         """Copy this step's status words to pinned memory behind an event."""
