@@ -135,6 +135,69 @@ __global__ void export_kernel(Geo g, StoreT<F> st, int64_t col0, int64_t col1,
     }
 }
 
+// Export of whole super cells, one CTA each: the CTA's records occupy one
+// contiguous output range (canonical order), so each array is staged in
+// shared memory -- threads scatter their column's records to their output
+// offsets there -- and written out with coalesced stores.  The column-per-
+// thread export_kernel writes 32 scattered records per warp store.
+template <typename F>
+__global__ void export_sc_kernel(Geo g, StoreT<F> st, int64_t col0, const int64_t *__restrict__ cell_start,
+                                 int clear, int32_t *cx, int32_t *cy, int32_t *cz, F *ox, F *oy,
+                                 F *oz, F *ux, F *uy, F *uz, F *w, int chunk) {
+    extern __shared__ __align__(16) unsigned char xs_raw[];
+    const int V = g.scx * g.scy * g.scz, K = st.frames, t = threadIdx.x;
+    const int64_t s = col0 / V + blockIdx.x;
+    const int64_t sc_first = s * V - col0;               // local index of this super cell's column 0
+    const int64_t S0 = cell_start[sc_first], S1 = cell_start[sc_first + V];
+    const bool owner = t < V;
+    int f = 0, b = 0;
+    int64_t my0 = 0;
+    int x = 0, y = 0, z = 0;
+    if (owner) {
+        const int64_t colx = s * V + t;
+        f = st.front[colx]; b = st.back[colx];
+        my0 = cell_start[sc_first + t];
+        const int bx = (int)(s % g.gx), by = (int)((s / g.gx) % g.gy), bz = (int)(s / ((int64_t)g.gx * g.gy));
+        x = bx * g.scx + t % g.scx; y = by * g.scy + (t / g.scx) % g.scy;
+        z = bz * g.scz + t / (g.scx * g.scy);
+    }
+    const int n = f + b;
+    F *bf = reinterpret_cast<F *>(xs_raw);
+    int32_t *bi = reinterpret_cast<int32_t *>(xs_raw);
+    for (int64_t base = S0; base < S1; base += chunk) {
+        const int64_t m = min((int64_t)chunk, S1 - base);
+        const int j0 = (int)max((int64_t)0, base - my0), j1 = (int)min((int64_t)n, base + chunk - my0);
+        // three cell arrays (constant per column), then the seven F arrays
+        for (int a = 0; a < 10; ++a) {
+            if (a < 3) {
+                const int v = a == 0 ? x : a == 1 ? y : z;
+                for (int j = j0; j < j1; ++j) bi[my0 + j - base] = v;
+            } else {
+                const F *src = a == 3 ? st.ox : a == 4 ? st.oy : a == 5 ? st.oz : a == 6 ? st.ux
+                             : a == 7 ? st.uy : a == 8 ? st.uz : st.w;
+                for (int j = j0; j < j1; ++j) {
+                    const int k = j < f ? j : K - b + (j - f);
+                    bf[my0 + j - base] = src[(s * K + k) * V + t];
+                }
+            }
+            __syncthreads();
+            if (a < 3) {
+                int32_t *dst = a == 0 ? cx : a == 1 ? cy : cz;
+                for (int i = t; i < m; i += blockDim.x) dst[base - cell_start[0] + i] = bi[i];
+            } else {
+                F *dst = a == 3 ? ox : a == 4 ? oy : a == 5 ? oz : a == 6 ? ux : a == 7 ? uy
+                       : a == 8 ? uz : w;
+                for (int i = t; i < m; i += blockDim.x) dst[base - cell_start[0] + i] = bf[i];
+            }
+            __syncthreads();
+        }
+    }
+    if (clear && owner) {
+        st.front[s * V + t] = 0;
+        st.back[s * V + t] = 0;
+    }
+}
+
 template <typename F>
 __global__ void repack_kernel(Geo g, StoreT<F> src, StoreT<F> dst) {
     const int V = g.scx * g.scy * g.scz, Ks = src.frames, Kd = dst.frames;
@@ -491,6 +554,26 @@ static int store_export(const kwb_grid *g, const kwb_store *st, int64_t col_begi
         return KWB_OK;
     }
     Geo geo = geo_of(*g);
+    const int V = g->scx * g->scy * g->scz;
+    if (capacity < 0 && col_begin % V == 0 && col_end % V == 0) {
+        // whole super cells: shared-memory staged, coalesced stores
+        const int64_t nsc = (col_end - col_begin) / V;
+        const int chunk = g->dtype == KWB_F32 ? 8192 : 4096;
+        const size_t smem = (size_t)chunk * (g->dtype == KWB_F32 ? 4 : 8);
+        const int th = block_threads(g);
+        if (g->dtype == KWB_F32) {
+            float *const *f = (float *const *)f7;
+            export_sc_kernel<float><<<(unsigned)nsc, th, smem, s>>>(
+                geo, store_of<float>(*st), col_begin, cell_start, clear, cx, cy, cz, f[0], f[1],
+                f[2], f[3], f[4], f[5], f[6], chunk);
+        } else {
+            double *const *f = (double *const *)f7;
+            export_sc_kernel<double><<<(unsigned)nsc, th, smem, s>>>(
+                geo, store_of<double>(*st), col_begin, cell_start, clear, cx, cy, cz, f[0], f[1],
+                f[2], f[3], f[4], f[5], f[6], chunk);
+        }
+        return kwb_check_launch("export_sc_kernel");
+    }
     const int64_t need = (col_end - col_begin + 255) / 256, cap = (int64_t)sm_count() * 16;
     const int blocks = (int)(need < cap ? need : cap);
     if (g->dtype == KWB_F32) {

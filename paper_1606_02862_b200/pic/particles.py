@@ -104,6 +104,18 @@ class SuperCellStore:
         return _Columns(self.n_super_cells, self.capacity, self.frames_per_sc, self.tdtype,
                         self.device)
 
+    def _reset_columns(self) -> None:
+        """Empty columns of frames_per_sc frames for a fresh load: buffers of
+        that size are reused (a restart keeps its ~GB allocations), others
+        are reallocated."""
+        keep = [c for c in self._cols if c is not None and c.frames == self.frames_per_sc]
+        if keep:
+            keep[0].front.zero_()
+            keep[0].back.zero_()
+            self._cols = [keep[0], keep[1] if len(keep) > 1 else None]
+        else:
+            self._cols = [self._new_columns(), None]
+
     @property
     def current(self) -> _Columns:
         return self._cols[0]
@@ -339,26 +351,32 @@ class SuperCellStore:
         d_f = [up(arrays[c], self.tdtype) for c in FLOAT_COLUMNS]
         n = d_cells[0].shape[0]
         nx, ny, nz = self.cells.as_tuple()
-        max_col = 0
         if n:
-            cx, cy, cz = (c.to(torch.int64) for c in d_cells)
-            lo = torch.stack([cx.min(), cy.min(), cz.min()])
-            hi = torch.stack([cx.max() - nx, cy.max() - ny, cz.max() - nz])
-            if int(lo.min().item()) < 0 or int(hi.max().item()) >= 0:
+            ext = torch.stack([t for c in d_cells for t in torch.aminmax(c)]).cpu()
+            lo, hi = ext[0::2], ext[1::2]
+            if int(lo.min()) < 0 or int(hi[0]) >= nx or int(hi[1]) >= ny or int(hi[2]) >= nz:
                 raise ContractViolation("particle cell index outside the grid")
+        # size the columns from the mean load (Poisson headroom, initial_frames);
+        # only if some column overflows is the fullest cell counted and the
+        # load redone (a histogram over all cells costs more than the load)
+        max_col = 0
+        for _attempt in range(2):
+            self.frames_per_sc = initial_frames(max_col, n / (nx * ny * nz))
+            self.loaded = n
+            self._reset_columns()
+            status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)
+            g = self._grid_struct()
+            _lib.call("kwb_store_load", _lib.ctypes.byref(g),
+                      _lib.ctypes.byref(self.current.cstruct()), n, d_cells[0].data_ptr(),
+                      d_cells[1].data_ptr(), d_cells[2].data_ptr(), _lib.ptr7(d_f),
+                      status.data_ptr(), _stream(stream, self.device))
+            bad = int(status[_lib.ST_LOAD_ERRORS].item())
+            if not bad:
+                return
+            cx, cy, cz = (c.to(torch.int64) for c in d_cells)
             cell = (cz * ny + cy) * nx + cx
             max_col = int(torch.bincount(cell, minlength=nx * ny * nz).max().item())
-        self.frames_per_sc = initial_frames(max_col, n / (nx * ny * nz))
-        self.loaded = n
-        self._cols = [self._new_columns(), None]
-        status = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int32, device=self.device)
-        g = self._grid_struct()
-        _lib.call("kwb_store_load", _lib.ctypes.byref(g), _lib.ctypes.byref(self.current.cstruct()),
-                  n, d_cells[0].data_ptr(), d_cells[1].data_ptr(), d_cells[2].data_ptr(),
-                  _lib.ptr7(d_f), status.data_ptr(), _stream(stream, self.device))
-        bad = int(status[_lib.ST_LOAD_ERRORS].item())
-        if bad:
-            raise AllocationError(f"{bad} particle record(s) could not be loaded")
+        raise AllocationError(f"{bad} particle record(s) could not be loaded")
 
     def init_device(self, params, species_index: int, seed: int, offsets=(0, 0, 0),
                     global_cells=None, stream=None) -> None:
@@ -370,7 +388,7 @@ class SuperCellStore:
         px, py, pz = _near_cubic_factors(ppc)
         n_cells = self.cells.volume
         self.frames_per_sc = initial_frames(ppc, float(ppc))
-        self._cols = [self._new_columns(), None]
+        self._reset_columns()
         gx, gy = (global_cells or self.cells.as_tuple())[:2]
         ini = _lib.InitC(ppc=ppc, px=px, py=py, pz=pz,
                          stream_velocity=params.stream_velocity,
