@@ -85,8 +85,12 @@ def shadow_error(orc, steps=1):
         return {n: 0.0 for n in FIELDS9}
     p32 = orc.params
     a = OracleSim(p32, validate=False, shape_order=orc.shape_order)
-    p64 = copy.copy(p32)
-    p64.dtype = np.dtype(np.float64)
+    import dataclasses
+    if dataclasses.is_dataclass(p32):   # SimParams is frozen
+        p64 = dataclasses.replace(p32, dtype=np.dtype(np.float64))
+    else:
+        p64 = copy.copy(p32)
+        p64.dtype = np.dtype(np.float64)
     b = OracleSim(p64, validate=False, shape_order=orc.shape_order)
     for so, sa, sb in zip(orc.stores, a.stores, b.stores):
         pk = so.packed()
