@@ -317,7 +317,8 @@ template <typename F, int ORDER>
 __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, int JV, int lane,
                                           int lx, int ly, int lz, int dcx, int dcy, int dcz,
                                           F oox, F ooy, F ooz, F nox, F noy, F noz, F w,
-                                          double fac0, double fac1, double fac2) {
+                                          double fac0, double fac1, double fac2,
+                                          bool skip_window) {
     using CT = F;
     constexpr int NP = Shape<ORDER>::NP, NS = NP - 1, NA = NP - 2;
     constexpr unsigned FULL = 0xffffffffu;
@@ -362,7 +363,15 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
             const CT s02 = __shfl_sync(FULL, s0, a2 * NS + j2);
             const CT ds2 = __shfl_sync(FULL, ds, a2 * NS + j2);
             const CT Pv = __shfl_sync(FULL, P, c * NS + ja);
-            if (p < npts) {
+            // entries of the owner cell's register window (own-relative edge
+            // -1..0, points -1..1; anchor-relative index j <-> own-relative
+            // j - 1 + m) were already added by deposit_window
+            const int mc = dcc < 0 ? -1 : 0;
+            const int m1 = (a1 == 0 ? dcx : a1 == 1 ? dcy : dcz) < 0 ? -1 : 0;
+            const int m2 = (a2 == 0 ? dcx : a2 == 1 ? dcy : dcz) < 0 ? -1 : 0;
+            const int e = ja - 1 + mc, p1 = j1 - 1 + m1, p2 = j2 - 1 + m2;
+            const bool inside = e >= -1 && e <= 0 && p1 >= -1 && p1 <= 1 && p2 >= -1 && p2 <= 1;
+            if (p < npts && !(skip_window && inside)) {
                 const CT T = u1 * s02 + v1 * ds2;
                 const CT val = Pv * T;
                 if (T != CT(0) && val != CT(0)) {
@@ -378,12 +387,16 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
 }
 
 // Deposit of a particle that crossed exactly one cell face, along axis k
-// (the common case: a two-axis crossing is ~40x rarer).  Axes are rotated so
-// the crossing axis is A0; with the anchor min(old, new) its supports span
-// indices 1..4, the other axes 1..3, and the footprint is exact:
+// (the common case: a two-axis crossing is ~40x rarer) -- the part of its
+// footprint OUTSIDE the owner cell's register window (deposit_window adds
+// the rest in registers).  Axes are rotated so the crossing axis is A0; with
+// the anchor min(old, new) its supports span indices 1..4, the other axes
+// 1..3; the full footprint is
 //   J_A0: along 1..3 x (A1: 1..3) x (A2: 1..3)  = 27 entries
 //   J_A1: along 1..2 x (A0: 1..4) x (A2: 1..3)  = 24 entries
 //   J_A2: along 1..2 x (A0: 1..4) x (A1: 1..3)  = 24 entries
+// of which the window holds 18 + 18 + 18: this routine adds the other
+// 9 + 6 + 6 (one along-edge of J_A0, one A0 point of J_A1 / J_A2).
 // (the transverse factor is symmetric in its two axes, so the reference's
 // per-component axis order does not matter).  TSC/CIC only.
 template <typename F, int ORDER>
@@ -421,19 +434,16 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
     {
         F *J = base + k * JV;
         const CT fw = (CT)(fac[k] * (double)w);
-        CT P[3];
-        P[0] = fw * dsc[0];
-        P[1] = fw * (dsc[0] + dsc[1]);
-        P[2] = fw * ((dsc[0] + dsc[1]) + dsc[2]);
+        // only the edge outside the owner's window: +k -> edge 3, -k -> edge 1
+        const int ja = m == 0 ? 2 : 0;
+        const CT Pout = m == 0 ? fw * ((dsc[0] + dsc[1]) + dsc[2]) : fw * dsc[0];
 #pragma unroll
         for (int j1 = 0; j1 < 3; ++j1) {
             const CT u = s0p[j1] + CT(0.5) * dsp[j1], v = CT(0.5) * s0p[j1] + dsp[j1] * CT(1.0 / 3.0);
 #pragma unroll
             for (int j2 = 0; j2 < 3; ++j2) {
                 const CT T = u * s0q[j2] + v * dsq[j2];
-                F *p = J + (j1 + 1) * s1_ + (j2 + 1) * s2_;
-#pragma unroll
-                for (int ja = 0; ja < 3; ++ja) atomicAdd(p + (ja + 1) * sk, (F)(P[ja] * T));
+                atomicAdd(J + (j1 + 1) * s1_ + (j2 + 1) * s2_ + (ja + 1) * sk, (F)(Pout * T));
             }
         }
     }
@@ -447,16 +457,16 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
         F *J = base + c * JV;
         const CT fw = (CT)(fac[c] * (double)w);
         const CT P0 = fw * dsa[0], P1 = fw * (dsa[0] + dsa[1]);
+        // only the point along k outside the owner's window: +k -> 4, -k -> 1
+        const int j1 = m == 0 ? 3 : 0;
+        const CT s0j = m == 0 ? s0c[3] : s0c[0], dsj = m == 0 ? dsc[3] : dsc[0];
+        const CT u = s0j + CT(0.5) * dsj, v = CT(0.5) * s0j + dsj * CT(1.0 / 3.0);
 #pragma unroll
-        for (int j1 = 0; j1 < 4; ++j1) {
-            const CT u = s0c[j1] + CT(0.5) * dsc[j1], v = CT(0.5) * s0c[j1] + dsc[j1] * CT(1.0 / 3.0);
-#pragma unroll
-            for (int j2 = 0; j2 < 3; ++j2) {
-                const CT T = u * s0o[j2] + v * dso[j2];
-                F *p = J + (j1 + 1) * sk + (j2 + 1) * so;
-                atomicAdd(p + sa, (F)(P0 * T));
-                atomicAdd(p + 2 * sa, (F)(P1 * T));
-            }
+        for (int j2 = 0; j2 < 3; ++j2) {
+            const CT T = u * s0o[j2] + v * dso[j2];
+            F *p = J + (j1 + 1) * sk + (j2 + 1) * so;
+            atomicAdd(p + sa, (F)(P0 * T));
+            atomicAdd(p + 2 * sa, (F)(P1 * T));
         }
     }
 }
@@ -531,32 +541,43 @@ struct RegAcc {
 };
 #endif
 
+// The window of every particle, crossing or not: the register accumulators
+// cover own-relative edges -1..0 along a component and points -1..1
+// transverse.  A particle that moved dc in {-1,0,1} on an axis has its new
+// shape on points dc-1..dc+1: the window sees it shifted (zero filled), and
+// for dc = -1 the along-axis running sum starts one point earlier (ds at
+// point -2).  For dc = 0 this is exactly the stayer deposit; the entries of
+// a crosser outside the window go through the queue (deposit_cross1 /
+// deposit_warp skip the window).
 template <int ORDER>
 __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, float ooz,
                                              float nox, float noy, float noz, float fwx,
-                                             float fwy, float fwz) {
-    float s0[3][3], ds[3][3];
+                                             float fwy, float fwz, int dcx, int dcy, int dcz) {
+    float s0[3][3], ds[3][3], dm2[3];
     {
-        float s1[3];
-        shape123f<ORDER>(oox, s0[0]);
-        shape123f<ORDER>(nox, s1);
+        const float oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
+        const int dc[3] = {dcx, dcy, dcz};
 #pragma unroll
-        for (int i = 0; i < 3; ++i) ds[0][i] = __fsub_rn(s1[i], s0[0][i]);
-        shape123f<ORDER>(ooy, s0[1]);
-        shape123f<ORDER>(noy, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[1][i] = __fsub_rn(s1[i], s0[1][i]);
-        shape123f<ORDER>(ooz, s0[2]);
-        shape123f<ORDER>(noz, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[2][i] = __fsub_rn(s1[i], s0[2][i]);
+        for (int a = 0; a < 3; ++a) {
+            float s1[3];
+            shape123f<ORDER>(oo[a], s0[a]);
+            shape123f<ORDER>(no[a], s1);
+            const float w0 = dc[a] == 0 ? s1[0] : (dc[a] > 0 ? 0.0f : s1[1]);
+            const float w1 = dc[a] == 0 ? s1[1] : (dc[a] > 0 ? s1[0] : s1[2]);
+            const float w2 = dc[a] == 0 ? s1[2] : (dc[a] > 0 ? s1[1] : 0.0f);
+            dm2[a] = dc[a] < 0 ? s1[0] : 0.0f;
+            ds[a][0] = __fsub_rn(w0, s0[a][0]);
+            ds[a][1] = __fsub_rn(w1, s0[a][1]);
+            ds[a][2] = __fsub_rn(w2, s0[a][2]);
+        }
     }
     const float fw[3] = {fwx, fwy, fwz};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;  // transverse axes: x:(y,z) y:(z,x) z:(x,y)
-        const float p1 = __fmul_rn(fw[c], ds[c][0]);
-        const float p2 = __fmul_rn(fw[c], __fadd_rn(ds[c][0], ds[c][1]));
+        const float r1 = __fadd_rn(dm2[c], ds[c][0]);
+        const float p1 = __fmul_rn(fw[c], r1);
+        const float p2 = __fmul_rn(fw[c], __fadd_rn(r1, ds[c][1]));
 #ifndef KWB_NO_FFMA2
         const unsigned long long P12 = RegAcc::pack(p1, p2);
 #endif
@@ -636,29 +657,33 @@ __device__ __forceinline__ void shape123d(double x, double (&s)[3]) {
 template <int ORDER>
 __device__ __forceinline__ void deposit_stay_d(RegAccD &R, double oox, double ooy, double ooz,
                                                double nox, double noy, double noz, double fwx,
-                                               double fwy, double fwz) {
-    double s0[3][3], ds[3][3];
+                                               double fwy, double fwz, int dcx, int dcy,
+                                               int dcz) {
+    double s0[3][3], ds[3][3], dm2[3];
     {
-        double s1[3];
-        shape123d<ORDER>(oox, s0[0]);
-        shape123d<ORDER>(nox, s1);
+        const double oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
+        const int dc[3] = {dcx, dcy, dcz};
 #pragma unroll
-        for (int i = 0; i < 3; ++i) ds[0][i] = s1[i] - s0[0][i];
-        shape123d<ORDER>(ooy, s0[1]);
-        shape123d<ORDER>(noy, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[1][i] = s1[i] - s0[1][i];
-        shape123d<ORDER>(ooz, s0[2]);
-        shape123d<ORDER>(noz, s1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ds[2][i] = s1[i] - s0[2][i];
+        for (int a = 0; a < 3; ++a) {
+            double s1[3];
+            shape123d<ORDER>(oo[a], s0[a]);
+            shape123d<ORDER>(no[a], s1);
+            const double w0 = dc[a] == 0 ? s1[0] : (dc[a] > 0 ? 0.0 : s1[1]);
+            const double w1 = dc[a] == 0 ? s1[1] : (dc[a] > 0 ? s1[0] : s1[2]);
+            const double w2 = dc[a] == 0 ? s1[2] : (dc[a] > 0 ? s1[1] : 0.0);
+            dm2[a] = dc[a] < 0 ? s1[0] : 0.0;
+            ds[a][0] = w0 - s0[a][0];
+            ds[a][1] = w1 - s0[a][1];
+            ds[a][2] = w2 - s0[a][2];
+        }
     }
     const double fw[3] = {fwx, fwy, fwz};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
-        const double p1 = fw[c] * ds[c][0];
-        const double p2 = fw[c] * (ds[c][0] + ds[c][1]);
+        const double r1 = dm2[c] + ds[c][0];
+        const double p1 = fw[c] * r1;
+        const double p2 = fw[c] * (r1 + ds[c][1]);
 #pragma unroll
         for (int j1 = 0; j1 < 3; ++j1) {
             const double u = __fma_rn(0.5, ds[a1][j1], s0[a1][j1]);
@@ -819,7 +844,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                                    ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
                                    q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
                                    q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                   q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                                   q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2], true);
         };
         if (!REGACC) {
             // PCS / float64: every particle is queued; one record per lane
@@ -968,16 +993,22 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #ifdef KWB_EXP_NODEPOSIT   // timing experiment only: no current deposit
             else if (true) { }
 #endif
-            else if (REGACC && dcx == 0 && dcy == 0 && dcz == 0) {
+            else if (REGACC) {
+                // the owner's register window, for crossers too; what a
+                // crosser deposits outside it goes through the queue
                 const double ww = (double)w;
                 if constexpr (sizeof(F) == 4)
                     deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox,
                                         (float)noy, (float)noz, (float)(sp.fac[0] * ww),
-                                        (float)(sp.fac[1] * ww), (float)(sp.fac[2] * ww));
+                                        (float)(sp.fac[1] * ww), (float)(sp.fac[2] * ww),
+                                        dcx, dcy, dcz);
                 else
                     deposit_stay_d<ORDER>(R, (double)ox, (double)oy, (double)oz, (double)nox,
                                           (double)noy, (double)noz, sp.fac[0] * ww,
-                                          sp.fac[1] * ww, sp.fac[2] * ww);
+                                          sp.fac[1] * ww, sp.fac[2] * ww, dcx, dcy, dcz);
+#ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
+                queue = (dcx | dcy | dcz) != 0;
+#endif
             } else {
 #ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
                 queue = true;
