@@ -82,6 +82,8 @@ def lib():
             build()
         L = ctypes.CDLL(_LIB_PATH)
         P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+        L.orc_div_rcp_check.argtypes = [I64, ctypes.c_uint64]
+        L.orc_div_rcp_check.restype = I64
         for sfx in ("_f32", "_f64"):
             getattr(L, "orc_gather" + sfx).argtypes = [P, P, I]
             getattr(L, "orc_push" + sfx).argtypes = [P, D, I]

@@ -110,3 +110,42 @@ void orc_unlink_empty(orc_pool *pl, int64_t n_sc) {
         }
     }
 }
+
+/* ---- test support: the GPU's shared-reciprocal division ------------------
+ * The CUDA advance computes the push's and the move's three quotients by one
+ * divisor as q0 = RN(a r), e = fma(-q0, b, a), q = e == 0 ? q0 : fma(e, r, q0)
+ * with r = RN(1 / b) (Markstein).  This checks that construction against
+ * IEEE a / b on n pseudo-random pairs drawn like the kernel's operands:
+ * numerators of either sign over 2^-40 .. 2^4 (including exact zeros of
+ * either sign), divisors over 1 .. 2^6.  Returns the number of pairs whose
+ * bit patterns differ.  C99 fma() is the same IEEE operation as __fma_rn. */
+static uint64_t orc_rng_next(uint64_t *s) {
+    uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+int64_t orc_div_rcp_check(int64_t n, uint64_t seed) {
+    int64_t bad = 0;
+    uint64_t st = seed;
+    for (int64_t i = 0; i < n; ++i) {
+        const uint64_t u1 = orc_rng_next(&st), u2 = orc_rng_next(&st), u3 = orc_rng_next(&st);
+        const double m1 = 1.0 + (double)(u1 >> 11) * 0x1.0p-53;         /* [1, 2) */
+        const double m2 = 1.0 + (double)(u2 >> 11) * 0x1.0p-53;
+        const int e1 = (int)(u3 % 45) - 40, e2 = (int)((u3 >> 8) % 7);
+        double a = ldexp(m1, e1), b = ldexp(m2, e2);
+        if ((u3 >> 16) & 1) a = -a;
+        if (((u3 >> 17) & 1023) == 0) a = ((u3 >> 27) & 1) ? -0.0 : 0.0;
+        const double r = 1.0 / b;
+        const double q0 = a * r;
+        const double e = fma(-q0, b, a);
+        const double q = e == 0.0 ? q0 : fma(e, r, q0);
+        const double ref = a / b;
+        uint64_t x, y;
+        memcpy(&x, &q, 8);
+        memcpy(&y, &ref, 8);
+        bad += x != y;
+    }
+    return bad;
+}

@@ -29,6 +29,20 @@ constexpr int kMaxCells = 256;            // super-cell volume limit = CTA size 
 constexpr int kWarps = kMaxCells / 32;
 constexpr int kWarpQ = 160;               // crossing-particle queue entries per warp
 
+// a / b correctly rounded from r = RN(1 / b) (one IEEE division): q0 =
+// RN(a r) is within 1 ulp of a / b, the residual a - b q0 is exact with an
+// FMA, and RN(q0 + r (a - b q0)) is the correctly rounded quotient
+// (Markstein's theorem) -- so the push's and the move's three quotients by
+// one divisor (gamma, 1 + t^2, gamma') cost one division each, bit for bit
+// the reference's a / b.  An exact q0 is returned as is (the FMA would turn
+// -0 into +0).  The theorem needs no overflow or subnormal intermediates:
+// the operands are O(1) momenta and fields over divisors >= 1.
+__device__ __forceinline__ double div_rcp(double a, double b, double r) {
+    const double q0 = a * r;
+    const double e = __fma_rn(-q0, b, a);
+    return e == 0.0 ? q0 : __fma_rn(e, r, q0);   // e == 0: q0 exact, keeps -0 / b = -0
+}
+
 // Yee staggers in cell units, pic/fields.py:24-31 (Ex Ey Ez Bx By Bz).
 __host__ __device__ constexpr double stagger(int c, int a) {
     return (c == 0) ? (a == 0 ? 1.0 : 0.5)
@@ -936,13 +950,15 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             const double umy = (double)uy + qe1;
             const double umz = (double)uz + qe2;
             const double gm = sqrt(((1.0 + umx * umx) + umy * umy) + umz * umz);
-            const double ttx = (qm * (double)b0) / gm;
-            const double tty = (qm * (double)b1) / gm;
-            const double ttz = (qm * (double)b2) / gm;
+            const double rgm = 1.0 / gm;
+            const double ttx = div_rcp(qm * (double)b0, gm, rgm);
+            const double tty = div_rcp(qm * (double)b1, gm, rgm);
+            const double ttz = div_rcp(qm * (double)b2, gm, rgm);
             const double tsq1 = 1.0 + ((ttx * ttx + tty * tty) + ttz * ttz);
-            const double ssx = (2.0 * ttx) / tsq1;
-            const double ssy = (2.0 * tty) / tsq1;
-            const double ssz = (2.0 * ttz) / tsq1;
+            const double rts = 1.0 / tsq1;
+            const double ssx = div_rcp(2.0 * ttx, tsq1, rts);
+            const double ssy = div_rcp(2.0 * tty, tsq1, rts);
+            const double ssz = div_rcp(2.0 * ttz, tsq1, rts);
             const double upx = umx + (umy * ttz - umz * tty);
             const double upy = umy + (umz * ttx - umx * ttz);
             const double upz = umz + (umx * tty - umy * ttx);
@@ -953,9 +969,10 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             // -- move (pic/kernels.py:107-135): gamma from F squares -------
             const F sxx = nux * nux, syy = nuy * nuy, szz = nuz * nuz;
             const double gv = sqrt(((1.0 + (double)sxx) + (double)syy) + (double)szz);
-            const double mpx = (double)ox + ((double)nux / gv) * sp.dt_d[0];
-            const double mpy = (double)oy + ((double)nuy / gv) * sp.dt_d[1];
-            const double mpz = (double)oz + ((double)nuz / gv) * sp.dt_d[2];
+            const double rgv = 1.0 / gv;
+            const double mpx = (double)ox + div_rcp((double)nux, gv, rgv) * sp.dt_d[0];
+            const double mpy = (double)oy + div_rcp((double)nuy, gv, rgv) * sp.dt_d[1];
+            const double mpz = (double)oz + div_rcp((double)nuz, gv, rgv) * sp.dt_d[2];
             const int dxi = (int)floor(mpx), dyi = (int)floor(mpy), dzi = (int)floor(mpz);
             nox = (F)(mpx - (double)dxi);
             noy = (F)(mpy - (double)dyi);

@@ -73,3 +73,12 @@ def test_kat_shapes_and_boris(oracle_lib):
     qm = q * dt / (2.0 * m)
     assert kat["boris_b0"][1] == u[1] and kat["boris_b0"][2] == u[2]
     assert kat["boris_b0"][0] == pytest.approx(u[0] + 2 * qm * e[0], abs=1e-16)
+
+
+def test_shared_reciprocal_division_is_ieee_division():
+    """The CUDA push/move divide three numerators by one divisor through
+    r = 1/b and a Markstein correction (csrc/advance.cuh div_rcp); bit for
+    bit IEEE a / b over 2^24 pairs drawn like the kernel's operands (C99
+    fma, the same IEEE operation as __fma_rn)."""
+    from oracle import pic as orc
+    assert orc.lib().orc_div_rcp_check(1 << 24, 12345) == 0
