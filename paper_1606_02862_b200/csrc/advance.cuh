@@ -12,9 +12,14 @@
 // Per-CTA shared memory:
 //   ebd   6 x (scx+2)(scy+2)(scz+2) float64  E/B + 1 guard cell, pre-widened
 //                                             (no per-particle F->D converts)
-//   jt    3 x (scx+2H)(scy+2H)(scz+2H) F      J tile incl. the shape halo
-//   queue kWarps x kWarpQ crossing records    (per warp, deposited after the
-//                                             main loop: no block barriers)
+//   jt    3 x (scx+2H)(scy+2H)(scz+2H) F      J tile incl. the shape halo; the
+//                                             register window of every cell is
+//                                             swept in, the queued remainder
+//                                             added with CAS
+//   queue kWarps x kWarpQ crossing records    (per warp: the out-of-window part
+//                                             of crossing particles, every
+//                                             particle for PCS; deposited after
+//                                             the main loop)
 //   arr   V int                               in-super-cell arrivals per cell
 //   pf    2 x 7 x 256 F                       next-particle records, cp.async
 //                                             (no registers held between rounds)
@@ -144,76 +149,15 @@ __device__ __forceinline__ void shape_anchor(CT x, CT (&s)[Shape<ORDER>::NP - 1]
     }
 }
 
-// Deposit of a particle that crossed a cell face (or of any particle on the
-// PCS / float64 paths) into the shared J tile, in the compute type CT
-// (float for float storage, double for double storage).  Per axis the
-// anchor is min(old cell, new cell), so old and new positions lie in [0, 2]
-// and every support fits indices 1..NS; the along-axis running sum stops at
-// NA = NP - 2 (its last entry -- the "closing" sum(s1) - sum(s0) -- is kept
-// only on axes the particle crossed; elsewhere it is a rounding residue).
-// Same density decomposition and transverse factor as pic/kernels.py:210-248
-// (factorised: T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2).  Shared
-// float atomics are CAS loops on sm_100a: this path is kept to the ~6 % of
-// particles that cross a face.
-template <typename F, int ORDER, typename CT>
-__device__ __noinline__ void deposit_cross(F *__restrict__ jt, int jx, int jy, int JV, int lx,
-                                           int ly, int lz, int dcx, int dcy, int dcz, F oox,
-                                           F ooy, F ooz, F nox, F noy, F noz, F w, double fac0,
-                                           double fac1, double fac2) {
-    constexpr int NP = Shape<ORDER>::NP, NS = NP - 1, NA = NP - 2;
-    const int dc[3] = {dcx, dcy, dcz};
-    const F oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
-    const CT fac[3] = {(CT)(fac0 * (double)w), (CT)(fac1 * (double)w), (CT)(fac2 * (double)w)};
-    CT s0[3][NS], ds[3][NS];
-    int nt[3], na[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const int m = dc[a] < 0 ? -1 : 0;
-        CT s1[NS];
-        shape_anchor<ORDER, CT>((CT)oo[a] - (CT)m, s0[a]);
-        shape_anchor<ORDER, CT>((CT)no[a] + (CT)(dc[a] - m), s1);
-#pragma unroll
-        for (int i = 0; i < NS; ++i) ds[a][i] = s1[i] - s0[a][i];
-        nt[a] = dc[a] != 0 ? NS : NS - 1;   // transverse support 1..nt
-        na[a] = dc[a] != 0 ? NA : NA - 1;   // along entries 1..na
-    }
-    const int ax = lx + min(dcx, 0), ay = ly + min(dcy, 0), az = lz + min(dcz, 0);
-    F *base = jt + (az * jy + ay) * jx + ax;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const int a1 = (c + 1) % 3, a2 = (c + 2) % 3;
-        CT P[NA];
-        CT run = CT(0);
-#pragma unroll
-        for (int i = 0; i < NA; ++i) { run += ds[c][i]; P[i] = fac[c] * run; }
-        F *Jc = base + c * JV;
-#pragma unroll
-        for (int j1 = 1; j1 <= NS; ++j1) {
-            if (j1 > nt[a1]) continue;
-            const CT u = s0[a1][j1 - 1] + CT(0.5) * ds[a1][j1 - 1];
-            const CT v = CT(0.5) * s0[a1][j1 - 1] + ds[a1][j1 - 1] * CT(1.0 / 3.0);
-#pragma unroll
-            for (int j2 = 1; j2 <= NS; ++j2) {
-                if (j2 > nt[a2]) continue;
-                const CT T = u * s0[a2][j2 - 1] + v * ds[a2][j2 - 1];
-                if (T == CT(0)) continue;
-#pragma unroll
-                for (int ja = 1; ja <= NA; ++ja) {
-                    if (ja > na[c]) continue;
-                    int o;
-                    if (c == 0) o = (j2 * jy + j1) * jx + ja;
-                    else if (c == 1) o = (j1 * jy + ja) * jx + j2;
-                    else o = (ja * jy + j2) * jx + j1;
-                    const CT val = P[ja - 1] * T;
-                    if (val != CT(0)) atomicAdd(Jc + o, (F)val);
-                }
-            }
-        }
-    }
-}
-
-// Compact form of deposit_cross for the kernels that queue every particle
-// (PCS, float64): the component and transverse-row loops are NOT unrolled
+// Deposit of a queued PCS particle into the shared J tile (PCS queues every
+// particle: 300 entries do not fit registers).  Per axis the anchor is
+// min(old cell, new cell), so old and new positions lie in [0, 2] and every
+// support fits indices 1..NS; the along-axis running sum stops at NA = NP - 2
+// (its last entry -- the "closing" sum(s1) - sum(s0) -- is kept only on
+// axes the particle crossed; elsewhere it is a rounding residue).  Same
+// density decomposition and transverse factor as pic/kernels.py:210-248
+// (factorised: T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2); shared float
+// atomics are CAS loops on sm_100a.  The component and transverse-row loops are NOT unrolled
 // -- the per-axis register arrays are rotated instead, so every index stays
 // a compile-time constant (no local memory) while the code is ~NS x NA CAS
 // sites instead of 3 x NS x NS x NA (the unrolled PCS routine is ~90 KB of
@@ -861,24 +805,16 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                                    q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2], true);
         };
         if (!REGACC) {
-            // PCS / float64: every particle is queued; one record per lane
-            // (PCS: the compact routine -- its unrolled form does not fit
-            // the instruction cache; CIC/TSC: unrolled)
+            // PCS: every particle is queued; one record per lane, loop-rolled
+            // routine (its unrolled form does not fit the instruction cache)
             for (int j = lane; j < wq; j += 32) {
                 const int info = q_info[j];
-                const int qx = info & 255, qy = (info >> 8) & 255, qz = (info >> 16) & 255;
-                const int ddx = ((info >> 24) & 3) - 1, ddy = ((info >> 26) & 3) - 1,
-                          ddz = ((info >> 28) & 3) - 1;
-                if (ORDER == 3)
-                    deposit_cross_compact<F, ORDER>(
-                        jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz, q_f[0 * QS + j],
-                        q_f[1 * QS + j], q_f[2 * QS + j], q_f[3 * QS + j], q_f[4 * QS + j],
-                        q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
-                else
-                    deposit_cross<F, ORDER, F>(
-                        jt, L.jx, L.jy, L.JV, qx, qy, qz, ddx, ddy, ddz, q_f[0 * QS + j],
-                        q_f[1 * QS + j], q_f[2 * QS + j], q_f[3 * QS + j], q_f[4 * QS + j],
-                        q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2]);
+                deposit_cross_compact<F, ORDER>(
+                    jt, L.jx, L.jy, L.JV, info & 255, (info >> 8) & 255, (info >> 16) & 255,
+                    ((info >> 24) & 3) - 1, ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
+                    q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j], q_f[3 * QS + j],
+                    q_f[4 * QS + j], q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0], sp.fac[1],
+                    sp.fac[2]);
             }
         } else {
             // single-axis crossers (the common case): one record per lane,
