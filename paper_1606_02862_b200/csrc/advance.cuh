@@ -455,31 +455,24 @@ __device__ __forceinline__ void shape123f(float x, float (&s)[3]) {
 // rounding residue, and is dropped.  fp32 with FMA: J is compared within
 // tolerance, never bitwise (the reference's own J order is not fixed).
 // The (ja = 1, ja = 2) pair of an entry shares T: one packed FFMA2
-// (fma.rn.f32x2, sm_100) updates both -- the same two round-to-nearest FMAs.
+// (__ffma2_rn, sm_100) updates both -- the same two round-to-nearest FMAs.
 #ifndef KWB_NO_FFMA2
 struct RegAcc {
-    unsigned long long p[3][3][3];  // [component][j1-1][j2-1] = {ja=1, ja=2} as f32x2
+    float2 p[3][3][3];  // [component][j1-1][j2-1] = {ja=1, ja=2}
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
             for (int b = 0; b < 3; ++b)
 #pragma unroll
-                for (int d = 0; d < 3; ++d) p[c][b][d] = 0ull;
+                for (int d = 0; d < 3; ++d) p[c][b][d] = make_float2(0.f, 0.f);
     }
     __device__ __forceinline__ float get(int c, int a, int b, int d) const {
-        float lo, hi;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p[c][b][d]));
-        return a == 0 ? lo : hi;
+        return a == 0 ? p[c][b][d].x : p[c][b][d].y;
     }
-    __device__ __forceinline__ static unsigned long long pack(float lo, float hi) {
-        unsigned long long r;
-        asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-        return r;
-    }
-    __device__ __forceinline__ void fma2(int c, int b, int d, unsigned long long P, float T) {
-        const unsigned long long TT = pack(T, T);   // folded into FFMA2's scalar operand
-        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(p[c][b][d]) : "l"(P), "l"(TT));
+    __device__ __forceinline__ static float2 pack(float lo, float hi) { return make_float2(lo, hi); }
+    __device__ __forceinline__ void fma2(int c, int b, int d, float2 P, float T) {
+        p[c][b][d] = __ffma2_rn(P, make_float2(T, T), p[c][b][d]);
     }
 };
 #else
@@ -537,26 +530,22 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
         const float p1 = __fmul_rn(fw[c], r1);
         const float p2 = __fmul_rn(fw[c], __fadd_rn(r1, ds[c][1]));
 #ifndef KWB_NO_FFMA2
-        const unsigned long long P12 = RegAcc::pack(p1, p2);
+        const auto P12 = RegAcc::pack(p1, p2);
 #endif
 #ifndef KWB_NO_FFMA2
         {   // T for j1 = 0, 1 as one f32x2 pair (same roundings), j1 = 2 scalar
-            const unsigned long long U01 = RegAcc::pack(__fmaf_rn(0.5f, ds[a1][0], s0[a1][0]),
-                                                        __fmaf_rn(0.5f, ds[a1][1], s0[a1][1]));
-            const unsigned long long V01 = RegAcc::pack(
+            const auto U01 = RegAcc::pack(__fmaf_rn(0.5f, ds[a1][0], s0[a1][0]),
+                                          __fmaf_rn(0.5f, ds[a1][1], s0[a1][1]));
+            const auto V01 = RegAcc::pack(
                 __fmaf_rn(1.0f / 3.0f, ds[a1][0], __fmul_rn(0.5f, s0[a1][0])),
                 __fmaf_rn(1.0f / 3.0f, ds[a1][1], __fmul_rn(0.5f, s0[a1][1])));
             const float u2 = __fmaf_rn(0.5f, ds[a1][2], s0[a1][2]);
             const float v2 = __fmaf_rn(1.0f / 3.0f, ds[a1][2], __fmul_rn(0.5f, s0[a1][2]));
 #pragma unroll
             for (int j2 = 0; j2 < 3; ++j2) {
-                unsigned long long vd, T01;
-                const unsigned long long S = RegAcc::pack(s0[a2][j2], s0[a2][j2]);
-                const unsigned long long D = RegAcc::pack(ds[a2][j2], ds[a2][j2]);
-                asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(vd) : "l"(V01), "l"(D));
-                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(T01) : "l"(U01), "l"(S), "l"(vd));
-                float T0, T1;
-                asm("mov.b64 {%0, %1}, %2;" : "=f"(T0), "=f"(T1) : "l"(T01));
+                const float2 vd = __fmul2_rn(V01, make_float2(ds[a2][j2], ds[a2][j2]));
+                const float2 T01 = __ffma2_rn(U01, make_float2(s0[a2][j2], s0[a2][j2]), vd);
+                const float T0 = T01.x, T1 = T01.y;
                 R.fma2(c, 0, j2, P12, T0);
                 R.fma2(c, 1, j2, P12, T1);
                 R.fma2(c, 2, j2, P12, __fmaf_rn(u2, s0[a2][j2], __fmul_rn(v2, ds[a2][j2])));
