@@ -447,6 +447,26 @@ __device__ __forceinline__ void shape123f(float x, float (&s)[3]) {
     }
 }
 
+// Old and new position of one axis at once (TSC: packed f32x2 arithmetic,
+// the same round-to-nearest operations as shape123f on each half).
+template <int ORDER>
+__device__ __forceinline__ void shape123f_pair(float xo, float xn, float (&so)[3], float (&sn)[3]) {
+    if (ORDER == 2) {
+        const float2 x = make_float2(xo, xn);
+        const float2 a = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-xo, -xn));
+        const float2 b = __fadd2_rn(x, make_float2(-0.5f, -0.5f));
+        const float2 h = make_float2(0.5f, 0.5f);
+        const float2 s0 = __fmul2_rn(h, __fmul2_rn(a, a));
+        const float2 s1 = __ffma2_rn(make_float2(-b.x, -b.y), b, make_float2(0.75f, 0.75f));
+        const float2 s2 = __fmul2_rn(h, __fmul2_rn(x, x));
+        so[0] = s0.x; so[1] = s1.x; so[2] = s2.x;
+        sn[0] = s0.y; sn[1] = s1.y; sn[2] = s2.y;
+    } else {
+        shape123f<ORDER>(xo, so);
+        shape123f<ORDER>(xn, sn);
+    }
+}
+
 // Register accumulation of a particle that stays in its cell (dc = 0):
 // J_a(ja, j1, j2) += P_ja * fw_a * T(j1, j2) for ja in {1, 2}, j1, j2 in
 // {1, 2, 3}, with P the running sum of ds along a and
@@ -511,8 +531,7 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             float s1[3];
-            shape123f<ORDER>(oo[a], s0[a]);
-            shape123f<ORDER>(no[a], s1);
+            shape123f_pair<ORDER>(oo[a], no[a], s0[a], s1);
             const float w0 = dc[a] == 0 ? s1[0] : (dc[a] > 0 ? 0.0f : s1[1]);
             const float w1 = dc[a] == 0 ? s1[1] : (dc[a] > 0 ? s1[0] : s1[2]);
             const float w2 = dc[a] == 0 ? s1[2] : (dc[a] > 0 ? s1[1] : 0.0f);
