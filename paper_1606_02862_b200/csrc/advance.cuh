@@ -716,6 +716,30 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         return;
     }
 
+    auto slot_of = [&](int i) -> int64_t {
+        const int k = i < front_in ? i : K - back_in + (i - front_in);
+        return ((int64_t)sc * K + k) * V + t;
+    };
+    // next-particle records are copied global -> shared asynchronously
+    // (double buffered, this thread's slots only) and read at their uses,
+    // so they occupy no registers between rounds
+    F *pf = reinterpret_cast<F *>(smem_raw + L.off_pf) + t;
+    auto prefetch = [&](int i) {
+        if (i < n_t) {
+            const int64_t q = slot_of(i);
+            F *d = pf + (i & 1) * 7 * kMaxCells;
+            cp_async_elem(d + 0 * kMaxCells, in.ox + q);
+            cp_async_elem(d + 1 * kMaxCells, in.oy + q);
+            cp_async_elem(d + 2 * kMaxCells, in.oz + q);
+            cp_async_elem(d + 3 * kMaxCells, in.ux + q);
+            cp_async_elem(d + 4 * kMaxCells, in.uy + q);
+            cp_async_elem(d + 5 * kMaxCells, in.uz + q);
+            cp_async_elem(d + 6 * kMaxCells, in.w + q);
+        }
+        cp_async_commit();
+    };
+    prefetch(0);   // issued before the staging: its latency overlaps it
+
     // ---- periodic index tables, then stage E/B and clear the J tile -------
     for (int i = t; i < L.tx; i += blockDim.x) wtx[i] = pymod(orgx - 1 + i, g.nx);
     for (int i = t; i < L.ty; i += blockDim.x) wty[i] = pymod(orgy - 1 + i, g.ny);
@@ -731,7 +755,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         // flat over (component, z, y, x) so every lane works, and batches of
         // kStageB independent loads in flight per thread (one memory latency
         // per batch instead of one per tile row)
-        constexpr int kStageB = 8;
+        constexpr int kStageB = 16;   // 6 x 600 values / 256 threads: one batch
         const int total = 6 * L.TV, nth = blockDim.x, txy_ = L.tx * L.ty;
         for (int base = t; base < total; base += kStageB * nth) {
             F v[kStageB];
@@ -775,29 +799,6 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     int n_err = 0;
     int wq = 0;      // this warp's queue fill (warp-uniform)
 
-    auto slot_of = [&](int i) -> int64_t {
-        const int k = i < front_in ? i : K - back_in + (i - front_in);
-        return ((int64_t)sc * K + k) * V + t;
-    };
-    // next-particle records are copied global -> shared asynchronously
-    // (double buffered, this thread's slots only) and read at their uses,
-    // so they occupy no registers between rounds
-    F *pf = reinterpret_cast<F *>(smem_raw + L.off_pf) + t;
-    auto prefetch = [&](int i) {
-        if (i < n_t) {
-            const int64_t q = slot_of(i);
-            F *d = pf + (i & 1) * 7 * kMaxCells;
-            cp_async_elem(d + 0 * kMaxCells, in.ox + q);
-            cp_async_elem(d + 1 * kMaxCells, in.oy + q);
-            cp_async_elem(d + 2 * kMaxCells, in.oz + q);
-            cp_async_elem(d + 3 * kMaxCells, in.ux + q);
-            cp_async_elem(d + 4 * kMaxCells, in.uy + q);
-            cp_async_elem(d + 5 * kMaxCells, in.uz + q);
-            cp_async_elem(d + 6 * kMaxCells, in.w + q);
-        }
-        cp_async_commit();
-    };
-    prefetch(0);
 
     // Deposit the queued crossing particles of this warp (lanes take one
     // record each; CAS into the J tile).
