@@ -1064,8 +1064,32 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     if (wq > 0) drain_queue();
     __syncthreads();
 
-    // ---- flush the J tile: coalesced red.global.add of non-zero rows ------
-    {
+    // ---- flush the J tile: coalesced red.global.add of non-zero entries ---
+    if (sizeof(F) == 4 && (L.jx & 1) == 0) {
+        // x-adjacent pairs with one red.global.add.v2.f32 where the pair is
+        // contiguous and 8-byte aligned in J (not across the periodic seam)
+        const int total = 3 * L.JV / 2, nth = blockDim.x, jxy = L.jx * L.jy;
+        for (int i2 = t; i2 < total; i2 += nth) {
+            const int i = 2 * i2;
+            const F v0 = jt[i], v1 = jt[i + 1];
+            if (v0 != F(0) || v1 != F(0)) {
+                const int c = i / L.JV, r = i - c * L.JV;
+                const int d = r / jxy, r2 = r - d * jxy;
+                const int b = r2 / L.jx, a = r2 - b * L.jx;
+                F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
+                F *row = dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
+                const int x0 = wjx[a], x1 = wjx[a + 1];
+                F *p0 = row + x0;
+                if (x1 == x0 + 1 && ((reinterpret_cast<uintptr_t>(p0) & 7) == 0)) {
+                    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p0), "f"((float)v0),
+                                 "f"((float)v1) : "memory");
+                } else {
+                    if (v0 != F(0)) atomicAdd(p0, v0);
+                    if (v1 != F(0)) atomicAdd(row + x1, v1);
+                }
+            }
+        }
+    } else {
         const int total = 3 * L.JV, nth = blockDim.x, jxy = L.jx * L.jy;
         for (int i = t; i < total; i += nth) {
             const F v = jt[i];
