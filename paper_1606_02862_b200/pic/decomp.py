@@ -137,6 +137,22 @@ class DistTransport:
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
+        # gloo moves host memory only: device tensors are staged through the
+        # host (functional multi-process tests on one GPU); NCCL moves them
+        # directly over NVLink
+        self.host_staging = dist.get_backend(group) == "gloo"
+
+    def _wire(self, x):
+        return x.cpu() if self.host_staging and x.is_cuda else x.contiguous()
+
+    def all_reduce(self, t, op=None):
+        op = self.dist.ReduceOp.SUM if op is None else op
+        if self.host_staging and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=op, group=self.group)
 
     def exchange(self, sends, recvs):
         dist = self.dist
@@ -144,10 +160,13 @@ class DistTransport:
         self_box = {(s, d, t): x for s, d, t, x in sends if d == me}
         ops = []
         for s, d, t, x in sorted((m for m in sends if m[1] != me), key=lambda m: (m[1], m[2])):
-            ops.append(dist.P2POp(dist.isend, x.contiguous(), d, self.group, t))
+            ops.append(dist.P2POp(dist.isend, self._wire(x), d, self.group, t))
         posted = []
         for s, d, t, x in sorted((m for m in recvs if m[0] != me), key=lambda m: (m[0], m[2])):
-            buf = x if x.is_contiguous() else torch.empty_like(x)
+            if self.host_staging and x.is_cuda:
+                buf = torch.empty(x.shape, dtype=x.dtype)
+            else:
+                buf = x if x.is_contiguous() else torch.empty_like(x)
             ops.append(dist.P2POp(dist.irecv, buf, s, self.group, t))
             posted.append((buf, x))
         for s, d, t, x in recvs:
@@ -325,9 +344,9 @@ class DecomposedSimulation:
         if isinstance(self.transport, DistTransport):
             dev = next(iter(self.locals.values())).device
             t = torch.tensor(tot[:3], dtype=torch.float64, device=dev)
-            self.transport.dist.all_reduce(t)
+            self.transport.all_reduce(t)
             m = torch.tensor([dmax], dtype=torch.float64, device=dev)
-            self.transport.dist.all_reduce(m, op=self.transport.dist.ReduceOp.MAX)
+            self.transport.all_reduce(m, op=self.transport.dist.ReduceOp.MAX)
             tot[:3] = t.cpu().numpy()
             tot[3] = float(m.item())
         p = self.params
@@ -343,7 +362,7 @@ class DecomposedSimulation:
         if isinstance(self.transport, DistTransport):
             dev = next(iter(self.locals.values())).device
             t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
-            self.transport.dist.all_reduce(t)
+            self.transport.all_reduce(t)
             return float(t.item())
         return float(v)
 
@@ -440,7 +459,7 @@ class DecomposedSimulation:
                 return
             over = torch.stack(flags).sum().to(torch.float64).reshape(1)
             if isinstance(self.transport, DistTransport):
-                self.transport.dist.all_reduce(over)
+                self.transport.all_reduce(over)
             if float(over.item()) == 0:
                 return
             # nothing of an overflowing range left its guard layer: clear the

@@ -1,0 +1,94 @@
+"""The z-slab decomposition as it runs on several GPUs -- one process per
+slab, DistTransport, the CUDA stores with the host-synchronisation-free
+guard exchange (kwb_store_extract / kwb_store_load_counted) -- exercised
+with two processes on the one GPU of this box.  The transport is gloo
+(tensors staged through the host), so no kernel of one rank ever waits on
+another rank; NCCL is the only piece not covered here.  Against a
+single-domain CUDA run of the same state: census, cells bitwise, particle
+state bitwise after the first step and within tolerance after, fields
+within tolerance; then a forced guard-message overflow redone by the
+all-reduced flag."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELDS9 = ("Ex", "Ey", "Ez", "Bx", "By", "Bz", "Jx", "Jy", "Jz")
+PK = ("cx", "cy", "cz", "ox", "oy", "oz", "ux", "uy", "uz", "w")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _sorted(pk):
+    keys = []
+    for k in reversed(PK):
+        a = np.asarray(pk[k])
+        keys.append(a.view(np.uint64 if a.itemsize == 8 else np.uint32) if a.dtype.kind == "f" else a)
+    o = np.lexsort(keys)
+    return {k: np.asarray(pk[k])[o] for k in PK}
+
+
+def _worker(rank, world, port, dtype, small_cap):
+    import torch
+    import torch.distributed as dist
+    from golden_util import rel_l2
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1606_02862_b200.pic import SimParams, default_species, init_khi
+        from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, DistTransport
+        p = SimParams(cells=(16, 16, 24), species=default_species(4, 4.0), particles_per_cell=4,
+                      dtype=np.dtype(dtype), stream_velocity=0.2, perturbation=0.05,
+                      thermal_u=0.3 if small_cap else 0.1)
+        ref = init_khi(p, seed=9, validate=False)
+        dec = DecomposedSimulation(p, world, [rank], DistTransport())
+        dec.load_global(particles=[st.packed() for st in ref.stores])
+        dec.refresh_guards()
+        if small_cap:
+            dec._xcap = 2
+        lay = dec.layouts[rank]
+        n0 = ref.census()
+        assert dec.census() == n0
+        tol = 1e-13 if np.dtype(dtype) == np.float64 else 1e-5
+        for t in range(3):
+            ref.step()
+            dec.step()
+            dec.check_status()
+            assert dec.census() == n0, "census not conserved across slabs"
+            for i, st in enumerate(ref.stores):
+                full = st.packed()
+                m = (full["cz"] >= lay.z0) & (full["cz"] < lay.z0 + lay.nzl)
+                mine = _sorted(dec.owned_particles(rank, i))
+                want = _sorted({k: v[m] for k, v in full.items()})
+                for k in ("cx", "cy", "cz"):
+                    np.testing.assert_array_equal(mine[k], want[k], err_msg=f"step {t} {k}")
+                for k in ("ox", "oy", "oz", "ux", "uy", "uz", "w"):
+                    if t == 0:
+                        np.testing.assert_array_equal(mine[k], want[k], err_msg=k)
+                    else:
+                        np.testing.assert_allclose(mine[k], want[k], rtol=100 * tol, atol=10 * tol)
+            for n in FIELDS9:
+                a = dec.owned_fields(rank, n)
+                b = ref.fields.numpy(n)[:, :, lay.z0:lay.z0 + lay.nzl]
+                assert rel_l2(a, b) <= tol * (1 + 10 * t) or np.abs(b).max() < 1e-30, (t, n)
+        if small_cap:
+            assert dec._xcap > 2, "the overflow was not detected"
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype,small_cap", [(np.float32, False), (np.float64, False),
+                                             (np.float32, True)])
+def test_two_processes_match_single_domain(dtype, small_cap):
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap), nprocs=2, join=True)
