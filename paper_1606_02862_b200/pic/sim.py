@@ -204,7 +204,10 @@ class Simulation:
                 f"{moved} particle(s) moved a full cell or more before deposit")
         self._enqueue_fields()
         self.step_count += 1
-        self.check_status()
+        # the field update does not touch the status words: apply the ones
+        # read above instead of a second synchronising read
+        self._drain_status()
+        self._apply_status(st)
 
     def enqueue_step(self):
         """Launch one full PIC cycle on the current stream without waiting for
