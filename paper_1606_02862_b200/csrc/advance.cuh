@@ -11,7 +11,8 @@
 //
 // Per-CTA shared memory:
 //   ebd   6 x (scx+2)(scy+2)(scz+2) float64  E/B + 1 guard cell, pre-widened
-//                                             (no per-particle F->D converts)
+//                                             (no per-particle F->D converts;
+//                                             float for float32 PCS, AdvCfg)
 //   jt    3 x (scx+2H)(scy+2H)(scz+2H) F      J tile incl. the shape halo; the
 //                                             register window of every cell is
 //                                             swept in, the queued remainder
@@ -32,7 +33,35 @@ struct FieldPtrs {
 
 constexpr int kMaxCells = 256;            // super-cell volume limit = CTA size limit
 constexpr int kWarps = kMaxCells / 32;
-constexpr int kWarpQ = 160;               // crossing-particle queue entries per warp
+#ifndef KWB_WARPQ
+#define KWB_WARPQ 160
+#endif
+constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per warp
+#ifndef KWB_WARPQ_PCS
+#define KWB_WARPQ_PCS 32
+#endif
+#ifndef KWB_MIN_BLOCKS
+#define KWB_MIN_BLOCKS 2
+#endif
+#ifndef KWB_MIN_BLOCKS_PCS
+#define KWB_MIN_BLOCKS_PCS 3
+#endif
+
+// Per-instance configuration.  The E/B tile is staged in float64 (no
+// per-particle converts in the gather) except for float32 PCS, which stages
+// the float fields as they are (the widening at the load is exact).  PCS
+// queues every particle, so its queue holds one round (drained every round)
+// instead of 160 records: 62 KB instead of 108 KB of shared memory, 3 CTAs
+// per SM instead of 2 -- more warps to hide its serial CAS chains (C4 PCS
+// advance 45.1 -> 37.1 ms; 80 registers with a few spills, measured).
+template <typename F, int ORDER>
+struct AdvCfg {
+    static constexpr bool kNarrowEB = ORDER == 3 && sizeof(F) == 4;
+    using EB = std::conditional_t<kNarrowEB, float, double>;
+    static constexpr int kQ = ORDER == 3 ? KWB_WARPQ_PCS : kWarpQ;
+    static constexpr int kMinBlocks =
+        sizeof(F) == 4 ? (ORDER == 3 ? KWB_MIN_BLOCKS_PCS : KWB_MIN_BLOCKS) : 1;
+};
 
 // a / b correctly rounded from r = RN(1 / b) (one IEEE division): q0 =
 // RN(a r) is within 1 ulp of a / b, the residual a - b q0 is exact with an
@@ -81,14 +110,15 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     AdvLayout L;
     L.tx = scx + 2; L.ty = scy + 2; L.tz = scz + 2; L.TV = L.tx * L.ty * L.tz;
     L.jx = scx + 2 * H; L.jy = scy + 2 * H; L.jz = scz + 2 * H; L.JV = L.jx * L.jy * L.jz;
-    size_t o = (size_t)6 * L.TV * sizeof(double);
+    using C = AdvCfg<F, ORDER>;
+    size_t o = (size_t)6 * L.TV * sizeof(typename C::EB);
     L.off_jt = o;
     o += (size_t)3 * L.JV * sizeof(F);
     o = (o + 15) & ~size_t(15);
     L.off_qf = o;
-    o += (size_t)7 * kWarps * kWarpQ * sizeof(F);
+    o += (size_t)7 * kWarps * C::kQ * sizeof(F);
     L.off_qi = o;
-    o += (size_t)kWarps * kWarpQ * sizeof(int);
+    o += (size_t)kWarps * C::kQ * sizeof(int);
     L.off_arr = o;
     o += (size_t)kMaxCells * sizeof(int);
     L.off_pf = o;
@@ -104,15 +134,15 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
 // shared by every component with the same stagger on that axis (CSE).
 // All eight corner loads are issued before the arithmetic (measured: the
 // compiler then overlaps them with the other components' math).
-template <int C>
-__device__ __forceinline__ double sample_tile(const double *__restrict__ T, double px, double py,
+template <int C, typename TT>
+__device__ __forceinline__ double sample_tile(const TT *__restrict__ T, double px, double py,
                                               double pz, int ox0, int oy0, int oz0, int tx,
                                               int txy) {
     const double ttx = px - stagger(C, 0), tty = py - stagger(C, 1), ttz = pz - stagger(C, 2);
     const int ix = (int)floor(ttx), iy = (int)floor(tty), iz = (int)floor(ttz);
     const double fx = ttx - (double)ix, fy = tty - (double)iy, fz = ttz - (double)iz;
     const int i00 = (iz - oz0) * txy + (iy - oy0) * tx + (ix - ox0);
-    const double *r00 = T + i00, *r10 = r00 + tx, *r01 = r00 + txy, *r11 = r01 + tx;
+    const TT *r00 = T + i00, *r10 = r00 + tx, *r01 = r00 + txy, *r11 = r01 + tx;
     const double a00 = r00[0], b00 = r00[1], a10 = r10[0], b10 = r10[1];   // (x, x+1) corners
     const double a01 = r01[0], b01 = r01[1], a11 = r11[0], b11 = r11[1];
     const double gx = 1.0 - fx;
@@ -675,10 +705,7 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
 
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
-#ifndef KWB_MIN_BLOCKS
-#define KWB_MIN_BLOCKS 2
-#endif
-__global__ void __launch_bounds__(kMaxCells, sizeof(F) == 4 ? KWB_MIN_BLOCKS : 1)
+__global__ void __launch_bounds__(kMaxCells, AdvCfg<F, ORDER>::kMinBlocks)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
                int32_t *__restrict__ status) {
     constexpr int H = Shape<ORDER>::H;
@@ -696,11 +723,13 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     const int orgx = bx * scx, orgy = by * scy, orgz = bz * scz;
     const int lx = t % scx, ly = (t / scx) % scy, lz = t / (scx * scy);
 
-    double *ebd = reinterpret_cast<double *>(smem_raw);
+    using EB = typename AdvCfg<F, ORDER>::EB;
+    constexpr int kQ = AdvCfg<F, ORDER>::kQ;
+    EB *ebd = reinterpret_cast<EB *>(smem_raw);
     F *jt = reinterpret_cast<F *>(smem_raw + L.off_jt);
-    F *q_f = reinterpret_cast<F *>(smem_raw + L.off_qf) + wid * kWarpQ;  // this warp's queue
-    int *q_info = reinterpret_cast<int *>(smem_raw + L.off_qi) + wid * kWarpQ;
-    constexpr int QS = kWarps * kWarpQ;                                  // column stride
+    F *q_f = reinterpret_cast<F *>(smem_raw + L.off_qf) + wid * kQ;  // this warp's queue
+    int *q_info = reinterpret_cast<int *>(smem_raw + L.off_qi) + wid * kQ;
+    constexpr int QS = kWarps * kQ;                                  // column stride
     int *arr = reinterpret_cast<int *>(smem_raw + L.off_arr);
     int *wtx = reinterpret_cast<int *>(smem_raw + L.off_wrap);
     int *wty = wtx + L.tx, *wtz = wty + L.ty, *wjx = wtz + L.tz, *wjy = wjx + L.jx,
@@ -777,7 +806,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #pragma unroll
             for (int u = 0; u < kStageB; ++u) {
                 const int i = base + u * nth;
-                if (i < total) ebd[i] = (double)v[u];
+                if (i < total) ebd[i] = (EB)v[u];
             }
         }
     }
@@ -793,7 +822,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
     const double cxd = (double)cx, cyd = (double)cy, czd = (double)cz;
     const int txy = L.tx * L.ty;
-    const double *EBx = ebd, *EBy = ebd + L.TV, *EBz = ebd + 2 * L.TV, *BBx = ebd + 3 * L.TV,
+    const EB *EBx = ebd, *EBy = ebd + L.TV, *EBz = ebd + 2 * L.TV, *BBx = ebd + 3 * L.TV,
                  *BBy = ebd + 4 * L.TV, *BBz = ebd + 5 * L.TV;
     int fo = 0;      // stayers written to the front of this column
     int n_err = 0;
@@ -989,7 +1018,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                         ((dcz + 1) << 28);
         }
         wq += __popc(qmask);
-        if (wq > kWarpQ - 32) {   // rare: the queue is normally drained after the loop
+        if (wq > kQ - 32) {   // rare: the queue is normally drained after the loop
             drain_queue();
             wq = 0;
         }
