@@ -38,7 +38,7 @@ constexpr int kWarps = kMaxCells / 32;
 #endif
 constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per warp
 #ifndef KWB_WARPQ_PCS
-#define KWB_WARPQ_PCS 32
+#define KWB_WARPQ_PCS 64
 #endif
 #ifndef KWB_MIN_BLOCKS
 #define KWB_MIN_BLOCKS 2
@@ -50,10 +50,11 @@ constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per
 // Per-instance configuration.  The E/B tile is staged in float64 (no
 // per-particle converts in the gather) except for float32 PCS, which stages
 // the float fields as they are (the widening at the load is exact).  PCS
-// queues every particle, so its queue holds one round (drained every round)
-// instead of 160 records: 62 KB instead of 108 KB of shared memory, 3 CTAs
-// per SM instead of 2 -- more warps to hide its serial CAS chains (C4 PCS
-// advance 45.1 -> 37.1 ms; 80 registers with a few spills, measured).
+// queues every particle, so its queue is a 64-record ring drained 32 at a
+// time (every lane busy) instead of 160 records: 70 KB instead of 108 KB of
+// shared memory, 3 CTAs per SM instead of 2 -- more warps to hide its
+// serial CAS chains (C4 PCS advance 45.1 -> 37.1 ms, ring 37.1 -> 35.4 ms;
+// 80 registers with a few spills, measured).
 template <typename F, int ORDER>
 struct AdvCfg {
     static constexpr bool kNarrowEB = ORDER == 3 && sizeof(F) == 4;
@@ -827,6 +828,11 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     int fo = 0;      // stayers written to the front of this column
     int n_err = 0;
     int wq = 0;      // this warp's queue fill (warp-uniform)
+    // PCS: the queue is a ring of kQ (a power of two) records from qh, and
+    // every full 32 are drained at once, so the drain's lanes are all busy
+    int qh = 0;
+    static_assert(REGACC || (kQ & (kQ - 1)) == 0, "PCS queue must be a power of two");
+    auto qidx = [&](int k) -> int { return REGACC ? k : (qh + k) & (kQ - 1); };
 
 
     // Deposit the queued crossing particles of this warp (lanes take one
@@ -845,7 +851,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         if (!REGACC) {
             // PCS: every particle is queued; one record per lane, loop-rolled
             // routine (its unrolled form does not fit the instruction cache)
-            for (int j = lane; j < wq; j += 32) {
+            for (int k = lane; k < wq; k += 32) {
+                const int j = qidx(k);
                 const int info = q_info[j];
                 deposit_cross_compact<F, ORDER>(
                     jt, L.jx, L.jy, L.JV, info & 255, (info >> 8) & 255, (info >> 16) & 255,
@@ -1010,7 +1017,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         // ---- crossing particles -> this warp's queue (no atomics) ---------
         const unsigned qmask = __ballot_sync(0xffffffffu, queue);
         if (queue) {
-            const int j = wq + __popc(qmask & ((1u << lane) - 1u));
+            const int j = qidx(wq + __popc(qmask & ((1u << lane) - 1u)));
             q_f[0 * QS + j] = ox; q_f[1 * QS + j] = oy; q_f[2 * QS + j] = oz;
             q_f[3 * QS + j] = nox; q_f[4 * QS + j] = noy; q_f[5 * QS + j] = noz;
             q_f[6 * QS + j] = w;
@@ -1018,7 +1025,15 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                         ((dcz + 1) << 28);
         }
         wq += __popc(qmask);
-        if (wq > kQ - 32) {   // rare: the queue is normally drained after the loop
+        if (!REGACC) {
+            if (wq >= 32) {   // PCS: one full record per lane
+                const int left = wq - 32;
+                wq = 32;
+                drain_queue();
+                qh = (qh + 32) & (kQ - 1);
+                wq = left;
+            }
+        } else if (wq > kQ - 32) {   // rare: the queue is normally drained after the loop
             drain_queue();
             wq = 0;
         }
