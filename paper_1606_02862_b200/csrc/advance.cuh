@@ -44,7 +44,7 @@ constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per
 #define KWB_MIN_BLOCKS 2
 #endif
 #ifndef KWB_MIN_BLOCKS_PCS
-#define KWB_MIN_BLOCKS_PCS 3
+#define KWB_MIN_BLOCKS_PCS 2
 #endif
 
 // Per-instance configuration.  The E/B tile is staged in float64 (no
@@ -53,8 +53,10 @@ constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per
 // queues every particle, so its queue is a 64-record ring drained 32 at a
 // time (every lane busy) instead of 160 records: 70 KB instead of 108 KB of
 // shared memory, 3 CTAs per SM instead of 2 -- more warps to hide its
-// serial CAS chains (C4 PCS advance 45.1 -> 37.1 ms, ring 37.1 -> 35.4 ms;
-// 80 registers with a few spills, measured).
+// serial CAS chains (C4 PCS advance 45.1 -> 37.1 ms, ring 37.1 -> 35.4 ms).
+// In the (8,8,4) instance the stayers then left the queue for the
+// atomic-free warp boxes (kBoxX; +40 KB, back to 2 CTAs per SM):
+// 35.4 -> 25.4 ms.
 template <typename F, int ORDER>
 struct AdvCfg {
     static constexpr bool kNarrowEB = ORDER == 3 && sizeof(F) == 4;
@@ -100,9 +102,26 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// PCS stayers (particles that keep their cell, ~95 % at C4) are deposited
+// without atomics into a warp-private box per J component: a warp of the
+// (8,8,4) super cell is 8 x 4 cells of one z plane, and its stayers'
+// footprints (edges -2..1 along the component, points -2..2 across) span
+// Jx 11x8x5, Jy 12x7x5, Jz 12x8x4 entries.  All lanes run the same entry
+// sequence; an instruction group only varies the entry's z offset, and
+// cells of one warp share z, so the lanes of a group never hit the same
+// entry (plain read-add-write, 4-5 independent per group); __syncwarp
+// orders consecutive groups.  The boxes are added into the J tile after
+// the loop (CAS, ~40 per thread).
+constexpr int kBoxX = 1244;          // 440 + 420 + 384 floats per warp
+constexpr int kBoxFloats = kBoxX;
+template <typename F, int ORDER>
+__host__ __device__ inline bool pcs_box_layout(int scx, int scy, int scz) {
+    return ORDER == 3 && sizeof(F) == 4 && scx == 8 && scy == 8 && scz == 4;
+}
+
 struct AdvLayout {
     int tx, ty, tz, TV, jx, jy, jz, JV;
-    size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, bytes;
+    size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, off_wb, bytes;
 };
 
 template <typename F, int ORDER>
@@ -126,6 +145,9 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     o += (size_t)2 * 7 * kMaxCells * sizeof(F);   // double-buffered next-particle records
     L.off_wrap = o;
     o += (size_t)(L.tx + L.ty + L.tz + L.jx + L.jy + L.jz) * sizeof(int);
+    o = (o + 15) & ~size_t(15);
+    L.off_wb = o;
+    if (pcs_box_layout<F, ORDER>(scx, scy, scz)) o += (size_t)kWarps * kBoxFloats * sizeof(F);
     L.bytes = (o + 15) & ~size_t(15);
     return L;
 }
@@ -704,6 +726,133 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
     return (oz * jy + oy) * jx + ox;
 }
 
+// One PCS stayer per lane into the warp's boxes (see kBoxX); every lane of
+// the warp calls this together (on = false: the lane adds nothing).  Same
+// density decomposition and factors as deposit_cross_compact with dc = 0
+// (pic/kernels.py:210-248, SURVEY.md §8c PCS).  (rx, ry) = cell relative to
+// the warp's 8 x 4 patch.
+// One group: all loads, then all stores (entries of a group never alias
+// across the warp's lanes), so the N read-add-writes overlap.
+template <int N>
+__device__ __forceinline__ void box_group(float *b, int stride, const float (&v)[N]) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+    float o[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o[i]) : "r"(a + 4u * i * stride) : "memory");
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u * i * stride), "f"(__fadd_rn(o[i], v[i]))
+                     : "memory");
+    __syncwarp();
+}
+__device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx, int ry, bool on,
+                                                float oox, float ooy, float ooz, float nox,
+                                                float noy, float noz, float w, double fac0,
+                                                double fac1, double fac2) {
+    float s0[3][5], ds[3][5], P[3][4];
+    {
+        // an idle lane's records may be stale bit patterns: never let them
+        // reach the arithmetic (0 * NaN would poison the box)
+        const float oo[3] = {on ? oox : 0.5f, on ? ooy : 0.5f, on ? ooz : 0.5f},
+                    no[3] = {on ? nox : 0.5f, on ? noy : 0.5f, on ? noz : 0.5f};
+        const double fac[3] = {fac0, fac1, fac2};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float a0[6], a1[6];
+            shape_anchor<3, float>(oo[a], a0);
+            shape_anchor<3, float>(no[a], a1);
+            const float fw = on ? (float)(fac[a] * (double)w) : 0.0f;   // w read only when on
+            float run = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                s0[a][i] = a0[i];
+                ds[a][i] = a1[i] - a0[i];
+                if (i < 4) { run += ds[a][i]; P[a][i] = fw * run; }
+            }
+        }
+    }
+    // Jx (along x; across y = j1, z = j2): groups over z; j1 rolled with
+    // rotated copies of the y arrays
+    {
+        float y0[5], y1[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) { y0[j] = s0[1][j]; y1[j] = ds[1][j]; }
+        float *b = box + rx + 11 * ry;
+#pragma unroll 1
+        for (int j1 = 0; j1 < 5; ++j1) {
+            const float uu = y0[0] + 0.5f * y1[0], vv = 0.5f * y0[0] + y1[0] * (1.0f / 3.0f);
+            float T[5];
+#pragma unroll
+            for (int j2 = 0; j2 < 5; ++j2) T[j2] = uu * s0[2][j2] + vv * ds[2][j2];
+#pragma unroll
+            for (int ja = 0; ja < 4; ++ja) {
+                float v[5];
+#pragma unroll
+                for (int j2 = 0; j2 < 5; ++j2) v[j2] = P[0][ja] * T[j2];
+                box_group<5>(b + ja, 11 * 8, v);
+            }
+            b += 11;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { y0[j] = y0[j + 1]; y1[j] = y1[j + 1]; }
+        }
+    }
+    // Jy (along y; across z = j1, x = j2): groups over z; j2 rolled with
+    // rotated copies of the x arrays
+    {
+        float uz[5], vz[5], x0[5], x1[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            uz[j] = s0[2][j] + 0.5f * ds[2][j];
+            vz[j] = 0.5f * s0[2][j] + ds[2][j] * (1.0f / 3.0f);
+            x0[j] = s0[0][j]; x1[j] = ds[0][j];
+        }
+        float *b = box + 440 + rx + 12 * ry;
+#pragma unroll 1
+        for (int j2 = 0; j2 < 5; ++j2) {
+            float T[5];
+#pragma unroll
+            for (int j1 = 0; j1 < 5; ++j1) T[j1] = uz[j1] * x0[0] + vz[j1] * x1[0];
+#pragma unroll
+            for (int ja = 0; ja < 4; ++ja) {
+                float v[5];
+#pragma unroll
+                for (int j1 = 0; j1 < 5; ++j1) v[j1] = P[1][ja] * T[j1];
+                box_group<5>(b + 12 * ja, 12 * 7, v);
+            }
+            b += 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { x0[j] = x0[j + 1]; x1[j] = x1[j + 1]; }
+        }
+    }
+    // Jz (along z; across x = j1, y = j2): groups over the along-z edges;
+    // j1 rolled with rotated copies of the x factors
+    {
+        float ux[5], vx[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            ux[j] = s0[0][j] + 0.5f * ds[0][j];
+            vx[j] = 0.5f * s0[0][j] + ds[0][j] * (1.0f / 3.0f);
+        }
+        float *b = box + 860 + rx + 12 * ry;
+#pragma unroll 1
+        for (int j1 = 0; j1 < 5; ++j1) {
+            const float uu = ux[0], vv = vx[0];
+#pragma unroll
+            for (int j2 = 0; j2 < 5; ++j2) {
+                const float T = uu * s0[1][j2] + vv * ds[1][j2];
+                float v[4];
+#pragma unroll
+                for (int ja = 0; ja < 4; ++ja) v[ja] = P[2][ja] * T;
+                box_group<4>(b + 12 * j2, 12 * 8, v);
+            }
+            b += 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { ux[j] = ux[j + 1]; vx[j] = vx[j + 1]; }
+        }
+    }
+}
+
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
 __global__ void __launch_bounds__(kMaxCells, AdvCfg<F, ORDER>::kMinBlocks)
@@ -780,6 +929,10 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     if (t < kMaxCells) arr[t] = 0;
     if (t == 0) s_maxcol = 0;
     for (int i = t; i < 3 * L.JV; i += blockDim.x) jt[i] = F(0);
+    constexpr bool PCSBOX = ORDER == 3 && !REGACC && sizeof(F) == 4 && SX == 8 && SY == 8 && SZ == 4;
+    float *wbox = reinterpret_cast<float *>(smem_raw + L.off_wb) + wid * kBoxFloats;
+    if constexpr (PCSBOX)
+        for (int i = lane; i < kBoxFloats; i += 32) wbox[i] = 0.0f;
     __syncthreads();
     {
         // flat over (component, z, y, x) so every lane works, and batches of
@@ -906,7 +1059,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         const F &ox = cur[0 * kMaxCells], &oy = cur[1 * kMaxCells], &oz = cur[2 * kMaxCells],
                 &ux = cur[3 * kMaxCells], &uy = cur[4 * kMaxCells], &uz = cur[5 * kMaxCells],
                 &w = cur[6 * kMaxCells];
-        bool queue = false, leave = false, mover = false, stay = false;
+        bool queue = false, leave = false, mover = false, stay = false, pstay = false;
         F nox = 0, noy = 0, noz = 0, nux = 0, nuy = 0, nuz = 0;
         int dcx = 0, dcy = 0, dcz = 0, ncx = 0, ncy = 0, ncz = 0, dest = 0, nlc = 0;
         if (active) {
@@ -1009,7 +1162,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #endif
             } else {
 #ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
-                queue = true;
+                if (PCSBOX && stay && (dcx | dcy | dcz) == 0) pstay = true;
+                else queue = true;
 #endif
             }
         }
@@ -1036,6 +1190,11 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         } else if (wq > kQ - 32) {   // rare: the queue is normally drained after the loop
             drain_queue();
             wq = 0;
+        }
+        if constexpr (PCSBOX) {   // PCS stayers: the warp's boxes, no atomics
+            if (__any_sync(0xffffffffu, pstay))
+                deposit_pcs_box(wbox, lx, ly - 4 * (wid & 1), pstay, ox, oy, oz, nox, noy, noz, w,
+                                sp.fac[0], sp.fac[1], sp.fac[2]);
         }
 
         // ---- write the particle to its column / the exchange --------------
@@ -1106,6 +1265,26 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     // (after the accumulator sweeps, when nothing else is live, so the
     // out-of-line deposit routines run without spilling the accumulators)
     if (wq > 0) drain_queue();
+    if constexpr (PCSBOX) {   // the warp's boxes into the J tile
+        __syncwarp();
+        const int y0 = 4 * (wid & 1), z0 = wid >> 1;
+        for (int e = lane; e < kBoxFloats; e += 32) {
+            const float v = wbox[e];
+            if (v != 0.0f) {
+                int c, X, Y, Z;
+                if (e < 440) {
+                    c = 0; X = e % 11; Y = (e / 11) % 8; Z = e / 88;
+                } else if (e < 860) {
+                    const int r = e - 440;
+                    c = 1; X = r % 12; Y = (r / 12) % 7; Z = r / 84;
+                } else {
+                    const int r = e - 860;
+                    c = 2; X = r % 12; Y = (r / 12) % 8; Z = r / 96;
+                }
+                atomicAdd(jt + c * L.JV + ((Z + z0 + 1) * L.jy + (Y + y0 + 1)) * L.jx + (X + 1), v);
+            }
+        }
+    }
     __syncthreads();
 
     // ---- flush the J tile: coalesced red.global.add of non-zero entries ---
