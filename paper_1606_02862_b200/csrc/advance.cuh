@@ -744,7 +744,7 @@ __device__ __forceinline__ void box_group(float *b, int stride, const float (&v)
     for (int i = 0; i < N; ++i)
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u * i * stride), "f"(__fadd_rn(o[i], v[i]))
                      : "memory");
-    __syncwarp();
+    __syncwarp();   // measured: without it lanes lose updates (tests/test_gpu_dense.py)
 }
 __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx, int ry, bool on,
                                                 float oox, float ooy, float ooz, float nox,
@@ -785,12 +785,14 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
             float T[5];
 #pragma unroll
             for (int j2 = 0; j2 < 5; ++j2) T[j2] = uu * s0[2][j2] + vv * ds[2][j2];
-#pragma unroll
+            float pa[4] = {P[0][0], P[0][1], P[0][2], P[0][3]};
+#pragma unroll 1
             for (int ja = 0; ja < 4; ++ja) {
                 float v[5];
 #pragma unroll
-                for (int j2 = 0; j2 < 5; ++j2) v[j2] = P[0][ja] * T[j2];
+                for (int j2 = 0; j2 < 5; ++j2) v[j2] = pa[0] * T[j2];
                 box_group<5>(b + ja, 11 * 8, v);
+                pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3];
             }
             b += 11;
 #pragma unroll
@@ -813,12 +815,14 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
             float T[5];
 #pragma unroll
             for (int j1 = 0; j1 < 5; ++j1) T[j1] = uz[j1] * x0[0] + vz[j1] * x1[0];
-#pragma unroll
+            float pa[4] = {P[1][0], P[1][1], P[1][2], P[1][3]};
+#pragma unroll 1
             for (int ja = 0; ja < 4; ++ja) {
                 float v[5];
 #pragma unroll
-                for (int j1 = 0; j1 < 5; ++j1) v[j1] = P[1][ja] * T[j1];
+                for (int j1 = 0; j1 < 5; ++j1) v[j1] = pa[0] * T[j1];
                 box_group<5>(b + 12 * ja, 12 * 7, v);
+                pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3];
             }
             b += 1;
 #pragma unroll
@@ -838,13 +842,18 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
 #pragma unroll 1
         for (int j1 = 0; j1 < 5; ++j1) {
             const float uu = ux[0], vv = vx[0];
+            float y0[5], y1[5];
 #pragma unroll
+            for (int j = 0; j < 5; ++j) { y0[j] = s0[1][j]; y1[j] = ds[1][j]; }
+#pragma unroll 1
             for (int j2 = 0; j2 < 5; ++j2) {
-                const float T = uu * s0[1][j2] + vv * ds[1][j2];
+                const float T = uu * y0[0] + vv * y1[0];
                 float v[4];
 #pragma unroll
                 for (int ja = 0; ja < 4; ++ja) v[ja] = P[2][ja] * T;
                 box_group<4>(b + 12 * j2, 12 * 8, v);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) { y0[j] = y0[j + 1]; y1[j] = y1[j + 1]; }
             }
             b += 1;
 #pragma unroll
