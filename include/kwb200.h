@@ -133,6 +133,22 @@ int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
                           void *const E[3], void *const B[3], void *const J[3],
                           int shape_order, int32_t *status, kwb_stream_t stream);
 
+/* kwb_particles_advance for one z-slab of a decomposed domain, with the J
+ * guard-plane halo sum fused into the deposit flush.  j_planes: DEVICE array
+ * of 3 * g->nz pointers (component-major); j_planes[c * nz + z] is the base
+ * of the nx*ny plane (x fastest) that local plane z of J[c] is added to.
+ * Owned planes point into J[c]; guard planes point into the z-neighbour's
+ * halo receive buffer (same-process memory, a peer pointer or a CUDA-IPC
+ * mapping), so no separate J halo message is sent.  NULL: plain J.
+ * Replaces the deposit + J-halo send of the reference's per-stage launch
+ * (pic/sim.py:138-163 DepositKernel; kw/atomics.py:147-163 atomic_add_dense
+ * for the wrapped tile rows). */
+int kwb_particles_advance_zslab(const kwb_grid *g, const kwb_species *sp,
+                                const kwb_store *in, const kwb_store *out,
+                                const kwb_exchange *ex, void *const E[3], void *const B[3],
+                                void *const J[3], void *const *j_planes, int shape_order,
+                                int32_t *status, kwb_stream_t stream);
+
 /* Super-cell shift: append the leavers in `ex` to the back of their new
  * columns in `out` (restores "every particle lives in its owning super cell"). */
 int kwb_particles_shift(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,

@@ -29,6 +29,11 @@
 struct FieldPtrs {
     const void *E[3], *B[3];
     void *J[3];
+    // optional [3][nz] base of every J z-plane (x fastest, nx*ny values):
+    // z-slab guard planes point into the neighbour's halo buffer (peer /
+    // IPC-mapped memory), so the J flush is also the halo exchange.  NULL:
+    // plane z of J[c].
+    void *const *jpl;
 };
 
 constexpr int kMaxCells = 256;            // super-cell volume limit = CTA size limit
@@ -1297,6 +1302,12 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     __syncthreads();
 
     // ---- flush the J tile: coalesced red.global.add of non-zero entries ---
+    auto jrow = [&](int c, int d, int b) -> F * {   // row (tile z d, tile y b) of J[c]
+        if (fp.jpl)
+            return (F *)fp.jpl[c * g.nz + wjz[d]] + (int64_t)wjy[b] * g.nx;
+        F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
+        return dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
+    };
     if (sizeof(F) == 4 && (L.jx & 1) == 0) {
         // x-adjacent pairs with one red.global.add.v2.f32 where the pair is
         // contiguous and 8-byte aligned in J (not across the periodic seam)
@@ -1308,8 +1319,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 const int c = i / L.JV, r = i - c * L.JV;
                 const int d = r / jxy, r2 = r - d * jxy;
                 const int b = r2 / L.jx, a = r2 - b * L.jx;
-                F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
-                F *row = dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
+                F *row = jrow(c, d, b);
                 const int x0 = wjx[a], x1 = wjx[a + 1];
                 F *p0 = row + x0;
                 if (x1 == x0 + 1 && ((reinterpret_cast<uintptr_t>(p0) & 7) == 0)) {
@@ -1329,8 +1339,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 const int c = i / L.JV, r = i - c * L.JV;
                 const int d = r / jxy, r2 = r - d * jxy;
                 const int b = r2 / L.jx, a = r2 - b * L.jx;
-                F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
-                atomicAdd(dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx + wjx[a], v);
+                atomicAdd(jrow(c, d, b) + wjx[a], v);
             }
         }
     }

@@ -380,8 +380,8 @@ static int block_threads(const kwb_grid *g) {
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
 static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex, void *const E[3],
-                          void *const B[3], void *const J[3], int32_t *status,
-                          cudaStream_t stream) {
+                          void *const B[3], void *const J[3], void *const *jpl,
+                          int32_t *status, cudaStream_t stream) {
     Geo geo = geo_of(*g);
     const int threads = block_threads(g);
     const size_t smem = adv_layout<F, ORDER>(g->scx, g->scy, g->scz).bytes;
@@ -394,6 +394,7 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     FieldPtrs fp;
     for (int c = 0; c < 3; ++c) { fp.E[c] = E[c]; fp.B[c] = B[c]; fp.J[c] = J[c]; }
+    fp.jpl = jpl;
     if (cudaMemsetAsync(ex->count, 0, sizeof(int32_t), stream) != cudaSuccess)
         return kwb_check_launch("exchange counter reset");
     const int n_sc = g->gx * g->gy * g->gz;
@@ -407,11 +408,11 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
 template <typename F, int ORDER, bool REGACC>
 static int dispatch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                             const kwb_store *out, const kwb_exchange *ex, void *const E[3],
-                            void *const B[3], void *const J[3], int32_t *status,
-                            cudaStream_t stream) {
+                            void *const B[3], void *const J[3], void *const *jpl,
+                            int32_t *status, cudaStream_t stream) {
     if (g->scx == 8 && g->scy == 8 && g->scz == 4)
-        return launch_advance<F, ORDER, REGACC, 8, 8, 4>(g, sp, in, out, ex, E, B, J, status, stream);
-    return launch_advance<F, ORDER, REGACC, 0, 0, 0>(g, sp, in, out, ex, E, B, J, status, stream);
+        return launch_advance<F, ORDER, REGACC, 8, 8, 4>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
+    return launch_advance<F, ORDER, REGACC, 0, 0, 0>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
 }
 
 extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
@@ -419,6 +420,17 @@ extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
                                      const kwb_exchange *ex, void *const E[3], void *const B[3],
                                      void *const J[3], int shape_order, int32_t *status,
                                      kwb_stream_t stream) {
+    return kwb_particles_advance_zslab(g, sp, in, out, ex, E, B, J, nullptr, shape_order, status,
+                                       stream);
+}
+
+extern "C" int kwb_particles_advance_zslab(const kwb_grid *g, const kwb_species *sp,
+                                           const kwb_store *in, const kwb_store *out,
+                                           const kwb_exchange *ex, void *const E[3],
+                                           void *const B[3], void *const J[3],
+                                           void *const *j_planes, int shape_order,
+                                           int32_t *status, kwb_stream_t stream) {
+    void *const *jpl = j_planes;
     int rc = check_grid(g);
     if (rc) return rc;
     if ((rc = check_store(in, "input")) || (rc = check_store(out, "output"))) return rc;
@@ -433,15 +445,15 @@ extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
     cudaStream_t s = (cudaStream_t)stream;
     if (g->dtype == KWB_F32) {
         switch (shape_order) {
-            case 1: return dispatch_advance<float, 1, true>(g, sp, in, out, ex, E, B, J, status, s);
-            case 2: return dispatch_advance<float, 2, true>(g, sp, in, out, ex, E, B, J, status, s);
-            case 3: return dispatch_advance<float, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 1: return dispatch_advance<float, 1, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 2: return dispatch_advance<float, 2, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 3: return dispatch_advance<float, 3, false>(g, sp, in, out, ex, E, B, J, jpl, status, s);
         }
     } else {
         switch (shape_order) {
-            case 1: return dispatch_advance<double, 1, true>(g, sp, in, out, ex, E, B, J, status, s);
-            case 2: return dispatch_advance<double, 2, true>(g, sp, in, out, ex, E, B, J, status, s);
-            case 3: return dispatch_advance<double, 3, false>(g, sp, in, out, ex, E, B, J, status, s);
+            case 1: return dispatch_advance<double, 1, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 2: return dispatch_advance<double, 2, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 3: return dispatch_advance<double, 3, false>(g, sp, in, out, ex, E, B, J, jpl, status, s);
         }
     }
     kwb_set_error("shape_order must be 1 (CIC), 2 (TSC) or 3 (PCS), got %d", shape_order);

@@ -115,6 +115,18 @@ def local_params(p: SimParams, lay: SlabLayout) -> SimParams:
                      perturbation=p.perturbation, thermal_u=p.thermal_u, shape=p.shape)
 
 
+def j_plane_owners(lay: SlabLayout):
+    """For every local plane z of slab `lay` (0 .. nze-1): (owner slab, its
+    local plane) of global plane global_z(z) -- the plane a deposit into
+    local plane z must land in.  Owned planes map to themselves."""
+    out = []
+    for zl in range(lay.nze):
+        gz = int(lay.global_z(zl))
+        o = gz // lay.nzl
+        out.append((o, gz - o * lay.nzl + lay.gp))
+    return out
+
+
 class LoopbackTransport:
     """All ranks in one process: messages are delivered by copies."""
 
@@ -186,7 +198,7 @@ class DecomposedSimulation:
     with LoopbackTransport."""
 
     def __init__(self, params: SimParams, world: int, ranks, transport, backend=None,
-                 local_factory=None):
+                 local_factory=None, fuse_j=None):
         self.params = params
         self.world = world
         self.transport = transport
@@ -203,8 +215,36 @@ class DecomposedSimulation:
         self.locals = {r: local_factory(local_params(params, lay))
                        for r, lay in self.layouts.items()}
         self.step_count = 0
+        # fused J halo: every slab's deposit flush adds its guard planes
+        # straight into the owning slab's J planes (kwb_particles_advance_zslab
+        # plane table), so the J guard-plane exchange disappears.  Needs every
+        # slab's J addressable from this process: all slabs driven by this
+        # process on one CUDA device (LoopbackTransport, or G = 1).  Across processes the same table would
+        # hold CUDA-IPC / peer pointers (not wired: one GPU here).
+        can_fuse = (len(self.layouts) == world
+                    and all(getattr(s, "device", torch.device("cpu")).type == "cuda"
+                            and hasattr(s, "_enqueue_particles")
+                            for s in self.locals.values()))
+        if fuse_j and not can_fuse:
+            raise ValueError("fuse_j needs every slab driven by this process on one CUDA "
+                             "device")
+        self.fuse_j = can_fuse if fuse_j is None else bool(fuse_j)
+        if self.fuse_j:
+            self._build_j_planes()
         self._xbuf = {}       # (rank, direction) -> fixed-capacity guard-exchange buffers
         self._xcap = None     # records per species per message
+
+    def _build_j_planes(self):
+        """Per slab a device table of 3 * nze plane base pointers: local J
+        plane z of component c -> the plane of the slab that owns global
+        plane global_z(z) (itself for owned planes, the z-neighbour -- or
+        itself across the periodic seam when G = 1 -- for guard planes)."""
+        for r, lay in self.layouts.items():
+            owners = j_plane_owners(lay)
+            ptrs = [self.locals[o].fields.storage(n)[oz].data_ptr()
+                    for n in J3 for o, oz in owners]
+            sim = self.locals[r]
+            sim._jplanes = torch.tensor(ptrs, dtype=torch.int64, device=sim.device)
 
     # -- state in / out --------------------------------------------------------
     def load_global(self, fields=None, particles=None):
@@ -285,10 +325,17 @@ class DecomposedSimulation:
         detected right away (one flag all-reduced per step) and the exchange
         redone with larger messages.  checked=False (enqueue_step): no host
         synchronisation at all; an overflow surfaces in check_status()."""
+        if self.fuse_j:
+            for sim in self.locals.values():
+                sim.fields.zero_current()
         for sim in self.locals.values():
             sim._drain_status(keep=1)
-            sim.advance_particles()
-        self._exchange_j()
+            if self.fuse_j:
+                sim.advance_particles(zero_j=False)
+            else:
+                sim.advance_particles()
+        if not self.fuse_j:
+            self._exchange_j()
         self._exchange_particles(checked)
         for sim in self.locals.values():
             sim.faraday_half()

@@ -284,19 +284,29 @@ class Simulation:
                       self._rho_prev.data_ptr(), None, self._J(), self._E(),
                       self._G_prev.data_ptr(), self._resid.data_ptr(), self._stream())
 
-    def _enqueue_particles(self):
+    def _enqueue_particles(self, zero_j=True):
+        """zero_j=False: J was zeroed by the caller (z-slab fused halo: other
+        slabs' deposits land in this slab's J before its own advance)."""
         stream = self._stream()
         g = ctypes.byref(self._grid)
-        self.fields.zero_current()
+        if zero_j:
+            self.fields.zero_current()
         self._status.zero_()
         E, B, J = self._E(), self._B(), self._J()
         ex = self._exchange_buffer()
+        jpl = getattr(self, "_jplanes", None)
         for i, st in enumerate(self.stores):
             src, dst = st.current, st.spare()
-            _lib.call("kwb_particles_advance", g, ctypes.byref(self._species[i]),
-                      ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
-                      ctypes.byref(ex.cstruct), E, B, J, self.shape_order,
-                      self._status[i].data_ptr(), stream)
+            if jpl is None:
+                _lib.call("kwb_particles_advance", g, ctypes.byref(self._species[i]),
+                          ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
+                          ctypes.byref(ex.cstruct), E, B, J, self.shape_order,
+                          self._status[i].data_ptr(), stream)
+            else:
+                _lib.call("kwb_particles_advance_zslab", g, ctypes.byref(self._species[i]),
+                          ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
+                          ctypes.byref(ex.cstruct), E, B, J, jpl.data_ptr(),
+                          self.shape_order, self._status[i].data_ptr(), stream)
             _lib.call("kwb_particles_shift", g, ctypes.byref(dst.cstruct()),
                       ctypes.byref(ex.cstruct), self._status[i].data_ptr(), stream)
             st.swap()
@@ -342,10 +352,10 @@ class Simulation:
         _lib.call("kwb_fields_ampere", ctypes.byref(self._grid), self._E(), self._B(),
                   self._J(), self.params.dt, self._stream())
 
-    def advance_particles(self):
+    def advance_particles(self, zero_j=True):
         """J = 0, then every species' fused advance + shift (the particle
         half of the cycle, pic/sim.py:138-163).  Asynchronous."""
-        self._enqueue_particles()
+        self._enqueue_particles(zero_j)
 
     def load_state(self, fields=None, particles=None):
         """Replace fields (name -> (nx, ny, nz) array) and/or particles (one

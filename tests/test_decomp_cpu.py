@@ -104,3 +104,28 @@ def test_layout_bookkeeping():
         SlabLayout(16, 16, 8, 4, 4, 0).validate()       # 2-plane slabs: not whole super cells
     with pytest.raises(ValueError):
         SlabLayout(16, 16, 13, 4, 2, 0).validate()      # not divisible
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_j_plane_owners_cover_every_plane(world):
+    """Fused J halo plane table (kwb_particles_advance_zslab): owned planes
+    map to themselves, guard planes to the neighbour's owned plane of the same
+    global z, and each global plane receives from exactly 1 + (guard copies)
+    local planes -- the same sums _exchange_j performs."""
+    from paper_1606_02862_b200.pic.decomp import SlabLayout, j_plane_owners
+    nz, scz = 8 * world, 4
+    lays = [SlabLayout(4, 4, nz, scz, world, r) for r in range(world)]
+    hits = np.zeros(nz, dtype=int)
+    for lay in lays:
+        own = lay.owned()
+        for zl, (o, oz) in enumerate(j_plane_owners(lay)):
+            olay = lays[o]
+            assert olay.owned().start <= oz < olay.owned().stop
+            assert int(olay.global_z(oz)) == int(lay.global_z(zl))
+            if own.start <= zl < own.stop:
+                assert (o, oz) == (lay.rank, zl)
+            hits[int(lay.global_z(zl))] += 1
+    # every global plane: its owner plus the guard planes that cover it
+    gp = lays[0].gp
+    assert hits.sum() == world * (nz // world + 2 * gp)
+    assert (hits >= 1).all()

@@ -24,16 +24,21 @@ def _sorted(pk):
     return {k: np.asarray(pk[k])[o] for k in PK}
 
 
+@pytest.mark.parametrize("fuse_j", [False, True])
 @pytest.mark.parametrize("world", [1, 2, 3])
 @pytest.mark.parametrize("dtype,shape", [(np.float64, "tsc"), (np.float32, "tsc"), (np.float32, "pcs")])
-def test_loopback_slabs_match_single_domain(world, dtype, shape):
+def test_loopback_slabs_match_single_domain(world, dtype, shape, fuse_j):
+    """fuse_j=True: guard-plane J deposited straight into the owning slab's
+    planes (kwb_particles_advance_zslab), no J exchange; False: the
+    exchanged-and-summed guard planes the multi-process path uses."""
     from paper_1606_02862_b200.pic import SimParams, default_species, init_khi
     from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
     p = SimParams(cells=(16, 16, 24), species=default_species(4, 4.0), particles_per_cell=4,
                   dtype=np.dtype(dtype), stream_velocity=0.2, perturbation=0.05, thermal_u=0.1,
                   shape=shape)
     ref = init_khi(p, seed=9, validate=False)
-    dec = DecomposedSimulation(p, world, range(world), LoopbackTransport())
+    dec = DecomposedSimulation(p, world, range(world), LoopbackTransport(), fuse_j=fuse_j)
+    assert dec.fuse_j == fuse_j
     dec.load_global(particles=[st.packed() for st in ref.stores])
     dec.refresh_guards()
     n0 = ref.census()
