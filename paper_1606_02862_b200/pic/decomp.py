@@ -166,6 +166,17 @@ class DistTransport:
         else:
             self.dist.all_reduce(t, op=op, group=self.group)
 
+    def device_barrier(self, device):
+        """Order this rank's stream after every rank's work enqueued so far
+        (NCCL: a one-element all-reduce the stream waits on, no host sync;
+        gloo: the host copy synchronises the stream first)."""
+        self.all_reduce(torch.zeros(1, dtype=torch.float32, device=device))
+
+    def all_gather_object(self, obj):
+        out = [None] * self.dist.get_world_size(self.group)
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
     def exchange(self, sends, recvs):
         dist = self.dist
         me = self.rank
@@ -221,7 +232,15 @@ class DecomposedSimulation:
         # slab's J addressable from this process: all slabs driven by this
         # process on one CUDA device (LoopbackTransport, or G = 1).  Across processes the same table would
         # hold CUDA-IPC / peer pointers (not wired: one GPU here).
-        can_fuse = (len(self.layouts) == world
+        on_cuda = all(getattr(s, "device", torch.device("cpu")).type == "cuda"
+                      and hasattr(s, "_enqueue_particles") for s in self.locals.values())
+        # fuse_j=True with one slab per process: the neighbours' J buffers are
+        # mapped through CUDA IPC (peer memory over NVLink on several GPUs) and
+        # two device barriers per step order the deposits (opt-in: only the
+        # two-processes-on-one-GPU case is tested here)
+        self._ipc = bool(fuse_j) and on_cuda and len(self.layouts) < world \
+            and isinstance(transport, DistTransport)
+        can_fuse = self._ipc or (len(self.layouts) == world
                     and all(getattr(s, "device", torch.device("cpu")).type == "cuda"
                             and hasattr(s, "_enqueue_particles")
                             for s in self.locals.values()))
@@ -239,10 +258,21 @@ class DecomposedSimulation:
         plane z of component c -> the plane of the slab that owns global
         plane global_z(z) (itself for owned planes, the z-neighbour -- or
         itself across the periodic seam when G = 1 -- for guard planes)."""
+        bufs = {r: self.locals[r].fields._buf for r in self.layouts}
+        if self._ipc:
+            # every rank exports its 9-lattice field buffer; the J planes of
+            # the z-neighbours are then plain device pointers in this process
+            from torch.multiprocessing.reductions import reduce_tensor
+            (r,) = self.layouts
+            handles = self.transport.all_gather_object(reduce_tensor(bufs[r]))
+            for o in {self.layouts[r].lower, self.layouts[r].upper} - {r}:
+                fn, args = handles[o]
+                bufs[o] = fn(*args)
+            self._peer_bufs = bufs      # keep the mappings alive
         for r, lay in self.layouts.items():
             owners = j_plane_owners(lay)
-            ptrs = [self.locals[o].fields.storage(n)[oz].data_ptr()
-                    for n in J3 for o, oz in owners]
+            ptrs = [bufs[o][6 + c][oz].data_ptr()
+                    for c in range(3) for o, oz in owners]
             sim = self.locals[r]
             sim._jplanes = torch.tensor(ptrs, dtype=torch.int64, device=sim.device)
 
@@ -328,12 +358,16 @@ class DecomposedSimulation:
         if self.fuse_j:
             for sim in self.locals.values():
                 sim.fields.zero_current()
+            if self._ipc:   # every neighbour's J is zero before anyone deposits
+                self.transport.device_barrier(next(iter(self.locals.values())).device)
         for sim in self.locals.values():
             sim._drain_status(keep=1)
             if self.fuse_j:
                 sim.advance_particles(zero_j=False)
             else:
                 sim.advance_particles()
+        if self._ipc:       # every deposit into this slab's J has landed
+            self.transport.device_barrier(next(iter(self.locals.values())).device)
         if not self.fuse_j:
             self._exchange_j()
         self._exchange_particles(checked)

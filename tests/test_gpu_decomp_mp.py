@@ -36,7 +36,7 @@ def _sorted(pk):
     return {k: np.asarray(pk[k])[o] for k in PK}
 
 
-def _worker(rank, world, port, dtype, small_cap):
+def _worker(rank, world, port, dtype, small_cap, fuse_j=False):
     import torch
     import torch.distributed as dist
     from golden_util import rel_l2
@@ -51,7 +51,8 @@ def _worker(rank, world, port, dtype, small_cap):
                       dtype=np.dtype(dtype), stream_velocity=0.2, perturbation=0.05,
                       thermal_u=0.3 if small_cap else 0.1)
         ref = init_khi(p, seed=9, validate=False)
-        dec = DecomposedSimulation(p, world, [rank], DistTransport())
+        dec = DecomposedSimulation(p, world, [rank], DistTransport(), fuse_j=fuse_j)
+        assert dec.fuse_j == fuse_j
         dec.load_global(particles=[st.packed() for st in ref.stores])
         dec.refresh_guards()
         if small_cap:
@@ -92,3 +93,13 @@ def _worker(rank, world, port, dtype, small_cap):
 def test_two_processes_match_single_domain(dtype, small_cap):
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap), nprocs=2, join=True)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_two_processes_fused_j_over_ipc(dtype):
+    """fuse_j=True across processes: each rank's deposit flush adds its guard
+    planes straight into the neighbour's J through a CUDA-IPC mapping (what
+    peer memory over NVLink does on several GPUs), ordered by two device
+    barriers per step; no J message is sent."""
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(2, _free_port(), dtype, False, True), nprocs=2, join=True)
