@@ -226,27 +226,24 @@ class DecomposedSimulation:
         self.locals = {r: local_factory(local_params(params, lay))
                        for r, lay in self.layouts.items()}
         self.step_count = 0
-        # fused J halo: every slab's deposit flush adds its guard planes
-        # straight into the owning slab's J planes (kwb_particles_advance_zslab
-        # plane table), so the J guard-plane exchange disappears.  Needs every
-        # slab's J addressable from this process: all slabs driven by this
-        # process on one CUDA device (LoopbackTransport, or G = 1).  Across processes the same table would
-        # hold CUDA-IPC / peer pointers (not wired: one GPU here).
+        # fused halo (fuse_j): every slab's deposit flush adds its J guard
+        # planes straight into the owning slab's J planes
+        # (kwb_particles_advance_zslab plane table) and the E/B guard refreshes
+        # are plane copies from the neighbours' buffers (_pull_guards): no J,
+        # E or B messages.  Default on when every slab is driven by this
+        # process on CUDA (LoopbackTransport, or G = 1).  fuse_j=True with one
+        # slab per process maps the neighbours' field buffers through CUDA IPC
+        # (peer memory over NVLink on several GPUs) and orders the peer
+        # accesses with device barriers; opt-in, as only the
+        # two-processes-on-one-GPU case ran here.
         on_cuda = all(getattr(s, "device", torch.device("cpu")).type == "cuda"
                       and hasattr(s, "_enqueue_particles") for s in self.locals.values())
-        # fuse_j=True with one slab per process: the neighbours' J buffers are
-        # mapped through CUDA IPC (peer memory over NVLink on several GPUs) and
-        # two device barriers per step order the deposits (opt-in: only the
-        # two-processes-on-one-GPU case is tested here)
         self._ipc = bool(fuse_j) and on_cuda and len(self.layouts) < world \
             and isinstance(transport, DistTransport)
-        can_fuse = self._ipc or (len(self.layouts) == world
-                    and all(getattr(s, "device", torch.device("cpu")).type == "cuda"
-                            and hasattr(s, "_enqueue_particles")
-                            for s in self.locals.values()))
+        can_fuse = self._ipc or (len(self.layouts) == world and on_cuda)
         if fuse_j and not can_fuse:
-            raise ValueError("fuse_j needs every slab driven by this process on one CUDA "
-                             "device")
+            raise ValueError("fuse_j needs CUDA slabs: all driven by this process, or one per "
+                             "process over DistTransport")
         self.fuse_j = can_fuse if fuse_j is None else bool(fuse_j)
         if self.fuse_j:
             self._build_j_planes()
@@ -268,7 +265,7 @@ class DecomposedSimulation:
             for o in {self.layouts[r].lower, self.layouts[r].upper} - {r}:
                 fn, args = handles[o]
                 bufs[o] = fn(*args)
-            self._peer_bufs = bufs      # keep the mappings alive
+        self._fbufs = bufs              # field buffers of this slab and its neighbours
         for r, lay in self.layouts.items():
             owners = j_plane_owners(lay)
             ptrs = [bufs[o][6 + c][oz].data_ptr()
@@ -618,7 +615,25 @@ class DecomposedSimulation:
                     self.locals[r].stores[i].append(rec, status=self.locals[r]._status[i])
                 o += m
 
+    def _pull_guards(self, lo, hi, sides):
+        """Fused E/B guards: after a device barrier (the neighbours' field
+        updates are complete), each slab copies the neighbours' boundary
+        owned planes of lattices [lo, hi) of the 9-lattice buffer straight
+        into its guard planes (peer reads over NVLink across processes);
+        no message, no staging buffer."""
+        if self._ipc:
+            self.transport.device_barrier(next(iter(self.locals.values())).device)
+        for r, lay in self.layouts.items():
+            dst = self._fbufs[r]
+            gp, nzl = lay.gp, lay.nzl
+            if "top" in sides:       # upper neighbour's first owned plane
+                dst[lo:hi, gp + nzl].copy_(self._fbufs[lay.upper][lo:hi, gp])
+            if "bottom" in sides:    # lower neighbour's last owned plane
+                dst[lo:hi, gp - 1].copy_(self._fbufs[lay.lower][lo:hi, gp + nzl - 1])
+
     def _exchange_e_top(self):
+        if self.fuse_j:
+            return self._pull_guards(0, 3, ("top",))
         sends, recvs, sets = [], [], []
         for r, lay in self.layouts.items():
             f = self.locals[r].fields
@@ -633,6 +648,8 @@ class DecomposedSimulation:
                 f.storage(n)[k].copy_(buf[c])
 
     def _exchange_guards(self):
+        if self.fuse_j:
+            return self._pull_guards(0, 6, ("top", "bottom"))
         sends, recvs, sets = [], [], []
         for r, lay in self.layouts.items():
             f = self.locals[r].fields
