@@ -482,8 +482,29 @@ class DecomposedSimulation:
                     cols = st.n_super_cells * st.capacity
                     per_guard = st.sc_grid.x * st.sc_grid.y * st.capacity * lay.ghost_layers
                     est = max(est, int(st.census() / max(cols, 1) * per_guard))
+            if isinstance(self.transport, DistTransport):
+                # every rank must size its messages alike (P2P pairs equal
+                # sizes; fused pulls read the peer's buffer): max over ranks
+                dev = next(iter(self.locals.values())).device
+                t = torch.tensor([float(est)], dtype=torch.float64, device=dev)
+                self.transport.all_reduce(t, op=self.transport.dist.ReduceOp.MAX)
+                est = int(t.item())
             self._xcap = max(4096, est // 8)
         return self._xcap
+
+    def _map_peer_messages(self):
+        """Fused halo across processes: CUDA-IPC map the z-neighbours' send
+        buffers (s_int, s_flt, s_cnt per direction) so that the receiver reads
+        them in place (collective: every rank (re)allocates them together)."""
+        from torch.multiprocessing.reductions import reduce_tensor
+        (r,) = self.layouts
+        mine = {d: [reduce_tensor(x) for x in self._xbuf[(r, d)][:3]] for d in (DOWN, UP)}
+        allh = self.transport.all_gather_object(mine)
+        lay = self.layouts[r]
+        self._peer_x = {}
+        for o in {lay.lower, lay.upper} - {r}:
+            for d in (DOWN, UP):
+                self._peer_x[(o, d)] = tuple(fn(*args) for fn, args in allh[o][d])
 
     def _exchange_particles_device(self, checked):
         """Guard-layer particles to the neighbour that owns them, with no host
@@ -499,6 +520,7 @@ class DecomposedSimulation:
             n_sp = len(self.params.species)
             flags = []
             sends, recvs, incoming = [], [], []
+            fresh = False
             for r, lay in self.layouts.items():
                 sim = self.locals[r]
                 dev, tdt = sim.device, sim.stores[0].tdtype
@@ -513,6 +535,7 @@ class DecomposedSimulation:
                             ((n_sp,), torch.int64), ((3, n_sp * cap), torch.int32),
                             ((7, n_sp * cap), tdt), ((n_sp,), torch.int64)))
                         self._xbuf[key] = buf
+                        fresh = True
                     s_int, s_flt, s_cnt, r_int, r_flt, r_cnt = buf
                     for i, st in enumerate(sim.stores):
                         per_layer = st.sc_grid.x * st.sc_grid.y * st.capacity
@@ -527,9 +550,27 @@ class DecomposedSimulation:
                     recvs += [(src, r, TAG_PCNT + direction, r_cnt),
                               (src, r, TAG_PINT + direction, r_int),
                               (src, r, TAG_PFLT + direction, r_flt)]
-                    incoming.append((sim, r_int, r_flt, r_cnt))
+                    incoming.append((sim, r_int, r_flt, r_cnt, src, direction))
                 flags.append(sim._status[:, _lib.ST_GUARD_OVERFLOW].sum())
-            self.transport.exchange(sends, recvs)
+            if self.fuse_j:
+                # fused halo: the receiver appends straight from the sender's
+                # send buffer (same process, or CUDA-IPC mapped after a device
+                # barrier: every rank's extract has completed) -- no message
+                if self._ipc:
+                    if fresh or getattr(self, "_peer_x", None) is None:
+                        self._map_peer_messages()
+                    self.transport.device_barrier(next(iter(self.locals.values())).device)
+                src_buf = {}
+                for sim, _, _, _, src, direction in incoming:
+                    if (src, direction) in self._xbuf:
+                        src_buf[(src, direction)] = self._xbuf[(src, direction)][:3]
+                    else:
+                        src_buf[(src, direction)] = self._peer_x[(src, direction)]
+                incoming = [(sim,) + tuple(src_buf[(src, d)][k] for k in (0, 1, 2))
+                            for sim, _, _, _, src, d in incoming]
+            else:
+                self.transport.exchange(sends, recvs)
+                incoming = [x[:4] for x in incoming]
             for sim, r_int, r_flt, r_cnt in incoming:
                 for i, st in enumerate(sim.stores):
                     st.append_counted(r_int, r_flt, r_cnt[i], cap, sim._status[i], offset=i * cap)

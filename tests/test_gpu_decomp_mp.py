@@ -95,11 +95,14 @@ def test_two_processes_match_single_domain(dtype, small_cap):
     mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap), nprocs=2, join=True)
 
 
-@pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_two_processes_fused_j_over_ipc(dtype):
+@pytest.mark.parametrize("dtype,small_cap", [(np.float32, False), (np.float64, False),
+                                             (np.float32, True)])
+def test_two_processes_fused_j_over_ipc(dtype, small_cap):
     """fuse_j=True across processes: each rank's deposit flush adds its guard
     planes straight into the neighbour's J through a CUDA-IPC mapping (what
     peer memory over NVLink does on several GPUs), ordered by two device
-    barriers per step; no J message is sent."""
+    barriers per step; no J message is sent.  E/B guards and the guard-layer
+    particles are likewise read in place from the neighbour's buffers
+    (small_cap: the overflow redo re-maps the doubled send buffers)."""
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(2, _free_port(), dtype, False, True), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap, True), nprocs=2, join=True)
