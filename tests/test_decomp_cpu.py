@@ -129,3 +129,19 @@ def test_j_plane_owners_cover_every_plane(world):
     gp = lays[0].gp
     assert hits.sum() == world * (nz // world + 2 * gp)
     assert (hits >= 1).all()
+
+
+def test_fuse_j_needs_cuda_slabs():
+    """fuse_j=True is refused for slabs without device memory (the oracle
+    locals): the plane table and peer mappings need CUDA buffers.  The
+    default (None) falls back to the message exchange."""
+    from oracle_slab import OracleLocal
+    from paper_1606_02862_b200.pic import SimParams, default_species
+    from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
+    p = SimParams(cells=(8, 8, 16), species=default_species(2, 4.0), particles_per_cell=2,
+                  dtype=np.dtype(np.float64))
+    with pytest.raises(ValueError, match="fuse_j"):
+        DecomposedSimulation(p, 2, range(2), LoopbackTransport(), local_factory=OracleLocal,
+                             fuse_j=True)
+    dec = DecomposedSimulation(p, 2, range(2), LoopbackTransport(), local_factory=OracleLocal)
+    assert dec.fuse_j is False
