@@ -262,9 +262,16 @@ class DecomposedSimulation:
             from torch.multiprocessing.reductions import reduce_tensor
             (r,) = self.layouts
             handles = self.transport.all_gather_object(reduce_tensor(bufs[r]))
+            mine = bufs[r].device
             for o in {self.layouts[r].lower, self.layouts[r].upper} - {r}:
                 fn, args = handles[o]
                 bufs[o] = fn(*args)
+                if bufs[o].device != mine:
+                    # the advance kernel red.adds into the peer's J from this
+                    # device: a cross-device copy makes torch enable peer
+                    # access mine -> peer (cudaDeviceEnablePeerAccess)
+                    torch.empty(1, dtype=bufs[o].dtype, device=mine).copy_(
+                        bufs[o].view(-1)[:1])
         self._fbufs = bufs              # field buffers of this slab and its neighbours
         for r, lay in self.layouts.items():
             owners = j_plane_owners(lay)
