@@ -36,7 +36,7 @@ def _sorted(pk):
     return {k: np.asarray(pk[k])[o] for k in PK}
 
 
-def _worker(rank, world, port, dtype, small_cap, fuse_j=False):
+def _worker(rank, world, port, dtype, small_cap, fuse_j=False, shape="tsc"):
     import torch
     import torch.distributed as dist
     from golden_util import rel_l2
@@ -49,7 +49,7 @@ def _worker(rank, world, port, dtype, small_cap, fuse_j=False):
         from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, DistTransport
         p = SimParams(cells=(16, 16, 24), species=default_species(4, 4.0), particles_per_cell=4,
                       dtype=np.dtype(dtype), stream_velocity=0.2, perturbation=0.05,
-                      thermal_u=0.3 if small_cap else 0.1)
+                      thermal_u=0.3 if small_cap else 0.1, shape=shape)
         ref = init_khi(p, seed=9, validate=False)
         dec = DecomposedSimulation(p, world, [rank], DistTransport(), fuse_j=fuse_j)
         assert dec.fuse_j == fuse_j
@@ -95,9 +95,12 @@ def test_two_processes_match_single_domain(dtype, small_cap):
     mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap), nprocs=2, join=True)
 
 
-@pytest.mark.parametrize("dtype,small_cap", [(np.float32, False), (np.float64, False),
-                                             (np.float32, True)])
-def test_two_processes_fused_j_over_ipc(dtype, small_cap):
+@pytest.mark.parametrize("dtype,small_cap,shape", [(np.float32, False, "tsc"),
+                                                   (np.float64, False, "tsc"),
+                                                   (np.float32, True, "tsc"),
+                                                   (np.float32, False, "pcs"),
+                                                   (np.float64, False, "cic")])
+def test_two_processes_fused_j_over_ipc(dtype, small_cap, shape):
     """fuse_j=True across processes: each rank's deposit flush adds its guard
     planes straight into the neighbour's J through a CUDA-IPC mapping (what
     peer memory over NVLink does on several GPUs), ordered by two device
@@ -105,4 +108,4 @@ def test_two_processes_fused_j_over_ipc(dtype, small_cap):
     particles are likewise read in place from the neighbour's buffers
     (small_cap: the overflow redo re-maps the doubled send buffers)."""
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap, True), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), dtype, small_cap, True, shape), nprocs=2, join=True)
