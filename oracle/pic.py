@@ -84,6 +84,10 @@ def lib():
         P, I64, D, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
         L.orc_div_rcp_check.argtypes = [I64, ctypes.c_uint64]
         L.orc_div_rcp_check.restype = I64
+        L.orc_div6_check.argtypes = [I64, ctypes.c_uint64]
+        L.orc_div6_check.restype = I64
+        L.orc_set_merge_seed.argtypes = [ctypes.c_uint64]
+        L.orc_set_reverse_slots.argtypes = [ctypes.c_int]
         for sfx in ("_f32", "_f64"):
             getattr(L, "orc_gather" + sfx).argtypes = [P, P, I]
             getattr(L, "orc_push" + sfx).argtypes = [P, D, I]
@@ -347,6 +351,8 @@ class OracleSim:
         self.validate = validate
         self.shape_order = int(shape_order)
         self.threads = threads or default_threads()
+        self.merge_seed = 0   # 0: Serial tile-merge order; else BlockPool-like permutation
+        self.reverse_slots = False   # particle order inside tiles (order-spread only)
         self.step_count = 0
         self.last_residual = 0.0
         cells = tuple(p.cells)
@@ -393,6 +399,8 @@ class OracleSim:
             self._fn("push")(ctypes.byref(cs), self.qm[i], nt)
             self._fn("move")(ctypes.byref(cs), *self.move_k, nx, ny, nz, nt)
             tiles = self._tiles_for(st.n_super_cells)
+            lib().orc_set_merge_seed(self.merge_seed + 7919 * i if self.merge_seed else 0)
+            lib().orc_set_reverse_slots(1 if self.reverse_slots else 0)
             err = self._fn("deposit")(ctypes.byref(cs), ctypes.byref(cf), self.shape_order,
                                       _p(self.fac[i]), *self.super_cell, _p(tiles), nt)
             if err:

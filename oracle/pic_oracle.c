@@ -13,6 +13,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #if defined(__FP_FAST_FMA) && !defined(ORACLE_ALLOW_FMA)
@@ -52,6 +53,22 @@ static const double ORC_STAGGER[6][3] = {
 };
 
 int orc_version(void) { return 1; }
+
+/* splitmix64 */
+static uint64_t orc_rng_next(uint64_t *s) {
+    uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* Tile merge order of the deposit: 0 = ascending super cells (the Serial
+ * back-end); otherwise the seed of a random permutation (BlockPool-like). */
+static uint64_t orc_merge_seed = 0;
+void orc_set_merge_seed(uint64_t seed) { orc_merge_seed = seed; }
+/* Particle order within each frame of a tile: 0 ascending slots (Serial). */
+static int orc_reverse_slots = 0;
+void orc_set_reverse_slots(int on) { orc_reverse_slots = on; }
 
 #define FT float
 #define SFX _f32
@@ -119,12 +136,6 @@ void orc_unlink_empty(orc_pool *pl, int64_t n_sc) {
  * numerators of either sign over 2^-40 .. 2^4 (including exact zeros of
  * either sign), divisors over 1 .. 2^6.  Returns the number of pairs whose
  * bit patterns differ.  C99 fma() is the same IEEE operation as __fma_rn. */
-static uint64_t orc_rng_next(uint64_t *s) {
-    uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
 
 int64_t orc_div_rcp_check(int64_t n, uint64_t seed) {
     int64_t bad = 0;
@@ -138,6 +149,30 @@ int64_t orc_div_rcp_check(int64_t n, uint64_t seed) {
         if ((u3 >> 16) & 1) a = -a;
         if (((u3 >> 17) & 1023) == 0) a = ((u3 >> 27) & 1) ? -0.0 : 0.0;
         const double r = 1.0 / b;
+        const double q0 = a * r;
+        const double e = fma(-q0, b, a);
+        const double q = e == 0.0 ? q0 : fma(e, r, q0);
+        const double ref = a / b;
+        uint64_t x, y;
+        memcpy(&x, &q, 8);
+        memcpy(&y, &ref, 8);
+        bad += x != y;
+    }
+    return bad;
+}
+
+/* The same construction for the PCS weights' a / 6 (csrc/advance.cuh div6:
+ * r = RN(1/6)) over non-negative numerators 2^-60 .. 4 and exact zero. */
+int64_t orc_div6_check(int64_t n, uint64_t seed) {
+    int64_t bad = 0;
+    uint64_t st = seed;
+    const double b = 6.0, r = 1.0 / 6.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const uint64_t u1 = orc_rng_next(&st), u3 = orc_rng_next(&st);
+        const double m1 = 1.0 + (double)(u1 >> 11) * 0x1.0p-53;
+        const int e1 = (int)(u3 % 62) - 60;
+        double a = ldexp(m1, e1);
+        if (((u3 >> 17) & 1023) == 0) a = 0.0;
         const double q0 = a * r;
         const double e = fma(-q0, b, a);
         const double q = e == 0.0 ? q0 : fma(e, r, q0);

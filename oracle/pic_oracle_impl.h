@@ -175,8 +175,13 @@ static int64_t CAT(deposit_sc, SFX)(const orc_store *st, int64_t sc, int order,
     int64_t errors = 0;
     const int64_t tplane = tnx * tny * tnz;
 #define T_(c, i, j, k) tile[(c) * tplane + ((i) * tny + (j)) * tnz + (k)]
+    /* orc_reverse_slots: walk each frame's slots backwards -- another valid
+     * particle order of the same super cell (the reference's order depends on
+     * its migration history), used only to measure the reference's own
+     * f32 accumulation-order spread (tests/parity_util.py order_spread). */
     for (int32_t f = st->head[sc]; f >= 0; f = st->next_f[f]) {
-        for (int64_t s = 0; s < st->cap; ++s) {
+        for (int64_t s_ = 0; s_ < st->cap; ++s_) {
+            const int64_t s = orc_reverse_slots ? st->cap - 1 - s_ : s_;
             int64_t q = (int64_t)f * st->cap + s;
             if (!st->occ[q]) continue;
             int64_t dcx = (int64_t)st->cx[q] - st->ocx[q];
@@ -276,7 +281,23 @@ int64_t ORC(deposit)(const orc_store *st, const orc_fields *fd, int order, const
     }
     if (errors) return errors;
     FT *J3[3] = {(FT *)fd->Jx, (FT *)fd->Jy, (FT *)fd->Jz};
-    for (int64_t sc = 0; sc < st->n_sc; ++sc) {
+    /* merge order: ascending (the Serial back-end, the bit-authoritative
+     * order) or, for orc_merge_seed != 0, a seeded random permutation -- the
+     * BlockPool back-end merges tiles in worker-completion order
+     * (kw/backends.py:115-139), which is how the reference's own J spread
+     * is measured (tests/parity_util.py order_spread). */
+    int64_t *perm = NULL;
+    if (orc_merge_seed) {
+        perm = (int64_t *)malloc(sizeof(int64_t) * st->n_sc);
+        uint64_t rs = orc_merge_seed;
+        for (int64_t i = 0; i < st->n_sc; ++i) perm[i] = i;
+        for (int64_t i = st->n_sc - 1; i > 0; --i) {
+            int64_t j = (int64_t)(orc_rng_next(&rs) % (uint64_t)(i + 1));
+            int64_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+        }
+    }
+    for (int64_t si = 0; si < st->n_sc; ++si) {
+        const int64_t sc = perm ? perm[si] : si;
         const FT *tile = tiles + sc * tsize;
         int64_t bx = sc % gx, by = (sc / gx) % gy, bz = sc / (gx * gy);
         for (int c = 0; c < 3; ++c) {
@@ -295,6 +316,7 @@ int64_t ORC(deposit)(const orc_store *st, const orc_fields *fd, int order, const
             }
         }
     }
+    free(perm);
     return 0;
 }
 

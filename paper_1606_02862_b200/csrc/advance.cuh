@@ -38,8 +38,21 @@ struct FieldPtrs {
 
 constexpr int kMaxCells = 256;            // super-cell volume limit = CTA size limit
 constexpr int kWarps = kMaxCells / 32;
+// KWB_WIN_SMEM: the float32 window's edge +1 (27 accumulators per thread)
+// lives in per-thread shared memory (7 float4 per thread, conflict-free)
+// instead of registers, so the kernel keeps 128 registers and 2 CTAs per SM
+// (C2 advance: 4.38 ms vs 4.80 ms with the spilling 81-register window and
+// 5.26 ms at one CTA per SM without spills; tools/gpurun/r02b.sh).
+// KWB_WIN_REGS=1 selects the all-register window.
+#if !defined(KWB_WIN_REGS) && !defined(KWB_WIN_SMEM)
+#define KWB_WIN_SMEM 1
+#endif
 #ifndef KWB_WARPQ
+#ifdef KWB_WIN_SMEM
+#define KWB_WARPQ 96
+#else
 #define KWB_WARPQ 160
+#endif
 #endif
 constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per warp
 #ifndef KWB_WARPQ_PCS
@@ -85,6 +98,67 @@ __device__ __forceinline__ double div_rcp(double a, double b, double r) {
     return e == 0.0 ? q0 : __fma_rn(e, r, q0);   // e == 0: q0 exact, keeps -0 / b = -0
 }
 
+// a / 6 correctly rounded (the PCS weights' division) by
+// div_rcp with r = RN(1/6): three fp64 operations instead of a division.
+__device__ __forceinline__ double div6(double a) {
+    return div_rcp(a, 6.0, 0.16666666666666666);
+}
+
+// ---- shape weights, bit for bit the reference's -------------------------
+// pic/kernels.py:138-150 `_shape5_into`: weight (F) W(|x - centre|) with x
+// and the distance in double, no contraction (the library is built with
+// --fmad=false); CIC/PCS per the SURVEY.md §8c extension.  Rounding the
+// weights to F only at the end is what keeps J within the reference's
+// tolerance: the f32-evaluated weights of round 1 differ by an ulp, and
+// ds = s1 - s0 turns that into ~1e-6 of J (profiles/r02_parity.md).
+template <int ORDER>
+__device__ __forceinline__ double wref(double d) {
+    if (ORDER == 2) {
+        const double e = 1.5 - d;
+        return d < 0.5 ? 0.75 - d * d : (d < 1.5 ? (0.5 * e) * e : 0.0);
+    } else if (ORDER == 1) {
+        return d < 1.0 ? 1.0 - d : 0.0;
+    } else {
+        const double e = 2.0 - d;
+        return d < 1.0 ? div6((4.0 - (6.0 * d) * d) + ((3.0 * d) * d) * d)
+                       : (d < 2.0 ? div6((e * e) * e) : 0.0);
+    }
+}
+
+// TSC/CIC weights at the three support points c-1, c, c+1 of a particle at
+// x in [c, c+1] (x = old offset with c = 0, or x = dc + new offset with
+// c = dc, exactly the reference's `(double)dc + (double)o`).  The distances
+// x - (c - 0.5), x - (c + 0.5), (c + 1.5) - x are the reference's |x -
+// centre| (signs known), and on these ranges the reference's branches
+// reduce to the three formulas below (the boundary cases d = 0.5 / 1.5 give
+// the same values), so each weight is the reference's bit for bit.
+template <int ORDER, typename F>
+__device__ __forceinline__ void wref3(double x, double c, F (&s)[3]) {
+    const double dl = x - (c - 0.5), dm = x - (c + 0.5), dh = (c + 1.5) - x;
+    if (ORDER == 2) {
+        const double el = 1.5 - dl, eh = 1.5 - dh;
+        s[0] = (F)((0.5 * el) * el);
+        s[1] = (F)(0.75 - dm * dm);
+        s[2] = (F)((0.5 * eh) * eh);
+    } else {
+        s[0] = (F)(dl < 1.0 ? 1.0 - dl : 0.0);
+        s[1] = (F)(1.0 - fabs(dm));
+        s[2] = (F)(dh < 1.0 ? 1.0 - dh : 0.0);
+    }
+}
+
+// Weight (F) at anchor-relative support index i (0-based) of the old and
+// the new position of one axis: the anchor is the old cell + m (m = -1 when
+// dc < 0), so index i is own-relative point i + 1 - H + m, centre + 0.5.
+template <int ORDER, typename F>
+__device__ __forceinline__ void wpair(F oo, F no, int dc, int m, int i, F &s0, F &s1) {
+    constexpr int H = Shape<ORDER>::H;
+    const double ctr = (double)(i + 1 - H + m) + 0.5;
+    const double xo = (double)oo, xn = (double)dc + (double)no;
+    s0 = (F)wref<ORDER>(fabs(xo - ctr));
+    s1 = (F)wref<ORDER>(fabs(xn - ctr));
+}
+
 // Yee staggers in cell units, pic/fields.py:24-31 (Ex Ey Ez Bx By Bz).
 __host__ __device__ constexpr double stagger(int c, int a) {
     return (c == 0) ? (a == 0 ? 1.0 : 0.5)
@@ -110,14 +184,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // PCS stayers (particles that keep their cell, ~95 % at C4) are deposited
 // without atomics into a warp-private box per J component: a warp of the
 // (8,8,4) super cell is 8 x 4 cells of one z plane, and its stayers'
-// footprints (edges -2..1 along the component, points -2..2 across) span
-// Jx 11x8x5, Jy 12x7x5, Jz 12x8x4 entries.  All lanes run the same entry
+// footprints (edges -2..2 along the component -- the last the closing
+// entry --, points -2..2 across) span Jx, Jy, Jz 12x8x5 entries each.  All lanes run the same entry
 // sequence; an instruction group only varies the entry's z offset, and
 // cells of one warp share z, so the lanes of a group never hit the same
 // entry (plain read-add-write, 4-5 independent per group); __syncwarp
 // orders consecutive groups.  The boxes are added into the J tile after
 // the loop (CAS, ~40 per thread).
-constexpr int kBoxX = 1244;          // 440 + 420 + 384 floats per warp
+constexpr int kBoxX = 1440;          // 3 x 480 floats per warp
 constexpr int kBoxFloats = kBoxX;
 template <typename F, int ORDER>
 __host__ __device__ inline bool pcs_box_layout(int scx, int scy, int scz) {
@@ -126,7 +200,7 @@ __host__ __device__ inline bool pcs_box_layout(int scx, int scy, int scz) {
 
 struct AdvLayout {
     int tx, ty, tz, TV, jx, jy, jz, JV;
-    size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, off_wb, bytes;
+    size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, off_wb, off_ws, bytes;
 };
 
 template <typename F, int ORDER>
@@ -153,6 +227,11 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     o = (o + 15) & ~size_t(15);
     L.off_wb = o;
     if (pcs_box_layout<F, ORDER>(scx, scy, scz)) o += (size_t)kWarps * kBoxFloats * sizeof(F);
+    o = (o + 15) & ~size_t(15);
+    L.off_ws = o;
+#ifdef KWB_WIN_SMEM
+    if (sizeof(F) == 4 && ORDER != 3) o += (size_t)7 * kMaxCells * sizeof(float4);
+#endif
     L.bytes = (o + 15) & ~size_t(15);
     return L;
 }
@@ -181,39 +260,17 @@ __device__ __forceinline__ double sample_tile(const TT *__restrict__ T, double p
     return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz;
 }
 
-// Shape weights at support indices 1..NS (NS = NP - 1) of a particle at
-// x in [0, 2] relative to an anchor cell: centres (i - H) + 0.5.  This is
-// the reference's _shape5_into (pic/kernels.py:138-150) for TSC, and the
-// SURVEY.md §8c CIC/PCS extension, evaluated in the compute type CT.
-template <int ORDER, typename CT>
-__device__ __forceinline__ void shape_anchor(CT x, CT (&s)[Shape<ORDER>::NP - 1]) {
-    constexpr int NP = Shape<ORDER>::NP, H = Shape<ORDER>::H;
-#pragma unroll
-    for (int i = 1; i < NP; ++i) {
-        CT d = x - (CT)((double)(i - H) + 0.5);
-        d = d < CT(0) ? -d : d;
-        CT v;
-        if (ORDER == 2) {
-            const CT e = CT(1.5) - d;
-            v = d < CT(0.5) ? CT(0.75) - d * d : (d < CT(1.5) ? CT(0.5) * e * e : CT(0));
-        } else if (ORDER == 1) {
-            v = d < CT(1) ? CT(1) - d : CT(0);
-        } else {
-            const CT e = CT(2) - d;
-            v = d < CT(1) ? (CT(4) - CT(6) * d * d + CT(3) * d * d * d) / CT(6)
-                          : (d < CT(2) ? e * e * e / CT(6) : CT(0));
-        }
-        s[i - 1] = v;
-    }
-}
-
 // Deposit of a queued PCS particle into the shared J tile (PCS queues every
 // particle: 300 entries do not fit registers).  Per axis the anchor is
 // min(old cell, new cell), so old and new positions lie in [0, 2] and every
-// support fits indices 1..NS; the along-axis running sum stops at NA = NP - 2
-// (its last entry -- the "closing" sum(s1) - sum(s0) -- is kept only on
-// axes the particle crossed; elsewhere it is a rounding residue).  Same
-// density decomposition and transverse factor as pic/kernels.py:210-248
+// support fits indices 1..NS; the along-axis running sum runs from the
+// reference's lo to its min(hi, NP - 2) -- NA entries, NA + 1 when the
+// particle moved down (pic/kernels.py:204-209, 221): its last entry is the
+// "closing" sum(s1) - sum(s0) unless the particle moved up, and it is kept
+// (a rounding residue of the F weights, but the reference deposits it and
+// without it f32 J misses the 1e-6 bar).  The running sums are exact
+// (double) so the residue is too.  Same density decomposition and
+// transverse factor as pic/kernels.py:210-248
 // (factorised: T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2); shared float
 // atomics are CAS loops on sm_100a.  The component and transverse-row loops are NOT unrolled
 // -- the per-axis register arrays are rotated instead, so every index stays
@@ -231,22 +288,23 @@ __device__ __noinline__ void deposit_cross_compact(F *__restrict__ jt, int jx, i
     const int dc[3] = {dcx, dcy, dcz};
     const F oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
     const double fac[3] = {fac0, fac1, fac2};
-    CT s0[3][NS], ds[3][NS], P[3][NA];
+    CT s0[3][NS], ds[3][NS], P[3][NS];
     int nt[3], na[3], st[3] = {1, jx, jx * jy};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const int m = dc[a] < 0 ? -1 : 0;
-        CT s1[NS];
-        shape_anchor<ORDER, CT>((CT)oo[a] - (CT)m, s0[a]);
-        shape_anchor<ORDER, CT>((CT)no[a] + (CT)(dc[a] - m), s1);
 #pragma unroll
-        for (int i = 0; i < NS; ++i) ds[a][i] = s1[i] - s0[a][i];
+        for (int i = 0; i < NS; ++i) {
+            CT s1;
+            wpair<ORDER, CT>(oo[a], no[a], dc[a], m, i, s0[a][i], s1);
+            ds[a][i] = s1 - s0[a][i];
+        }
         nt[a] = dc[a] != 0 ? NS : NS - 1;
-        na[a] = dc[a] != 0 ? NA : NA - 1;
-        const CT fw = (CT)(fac[a] * (double)w);
-        CT run = CT(0);
+        na[a] = NA - m;
+        const double fw = fac[a] * (double)w;
+        double run = 0.0;
 #pragma unroll
-        for (int i = 0; i < NA; ++i) { run += ds[a][i]; P[a][i] = fw * run; }
+        for (int i = 0; i < NS; ++i) { run += (double)ds[a][i]; P[a][i] = (CT)(fw * run); }
     }
     const int ax = lx + min(dcx, 0), ay = ly + min(dcy, 0), az = lz + min(dcz, 0);
     F *Jc = jt + (az * jy + ay) * jx + ax;
@@ -271,7 +329,7 @@ __device__ __noinline__ void deposit_cross_compact(F *__restrict__ jt, int jx, i
                     if (T != CT(0)) {
                         F *q = row + (j2 + 1) * s2_;
 #pragma unroll
-                        for (int ja = 0; ja < NA; ++ja) {
+                        for (int ja = 0; ja < NS; ++ja) {
                             const CT val = P[0][ja] * T;
                             if (ja < nac && val != CT(0)) atomicAdd(q + (ja + 1) * sa, (F)val);
                         }
@@ -286,13 +344,9 @@ __device__ __noinline__ void deposit_cross_compact(F *__restrict__ jt, int jx, i
         // rotate the axes: (c, c+1, c+2) -> (c+1, c+2, c+3)
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            const CT a0 = s0[0][j], b0 = ds[0][j];
+            const CT a0 = s0[0][j], b0 = ds[0][j], p0 = P[0][j];
             s0[0][j] = s0[1][j]; s0[1][j] = s0[2][j]; s0[2][j] = a0;
             ds[0][j] = ds[1][j]; ds[1][j] = ds[2][j]; ds[2][j] = b0;
-        }
-#pragma unroll
-        for (int j = 0; j < NA; ++j) {
-            const CT p0 = P[0][j];
             P[0][j] = P[1][j]; P[1][j] = P[2][j]; P[2][j] = p0;
         }
         { const int t0 = nt[0]; nt[0] = nt[1]; nt[1] = nt[2]; nt[2] = t0; }
@@ -310,25 +364,11 @@ __device__ __noinline__ void deposit_cross_compact(F *__restrict__ jt, int jx, i
 // per pass, each lane fetching its operands by shuffle and issuing one CAS.
 // Distinct lanes hit distinct entries, the code is a few hundred bytes (the
 // fully unrolled per-lane PCS routine is ~90 KB and thrashes the instruction
-// cache) and every lane is busy.  Same arithmetic as deposit_cross up to the
-// summation order of P (J is compared within tolerance).
-template <int ORDER, typename CT>
-__device__ __forceinline__ CT shape_point(CT x, int i) {
-    constexpr int H = Shape<ORDER>::H;
-    CT d = x - (CT)((double)(i + 1 - H) + 0.5);
-    d = d < CT(0) ? -d : d;
-    if (ORDER == 2) {
-        const CT e = CT(1.5) - d;
-        return d < CT(0.5) ? CT(0.75) - d * d : (d < CT(1.5) ? CT(0.5) * e * e : CT(0));
-    } else if (ORDER == 1) {
-        return d < CT(1) ? CT(1) - d : CT(0);
-    } else {
-        const CT e = CT(2) - d;
-        return d < CT(1) ? (CT(4) - CT(6) * d * d + CT(3) * d * d * d) / CT(6)
-                         : (d < CT(2) ? e * e * e / CT(6) : CT(0));
-    }
-}
-
+// cache) and every lane is busy.  Same arithmetic as deposit_cross_compact
+// up to the summation order of P (J is compared within tolerance).
+// Entries inside the owner's register window (deposit_window: own-relative
+// edges -1..+1 for float32; -1..0, and +1 where it is the closing residue,
+// for float64) are skipped.
 template <typename F, int ORDER>
 __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, int JV, int lane,
                                           int lx, int ly, int lz, int dcx, int dcy, int dcz,
@@ -337,6 +377,7 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
                                           bool skip_window) {
     using CT = F;
     constexpr int NP = Shape<ORDER>::NP, NS = NP - 1, NA = NP - 2;
+    constexpr bool PLUS = sizeof(F) == 4;
     constexpr unsigned FULL = 0xffffffffu;
     // this lane's support point
     const int a = lane / NS, i = lane - a * NS;
@@ -345,16 +386,17 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
     const F noa = a == 0 ? nox : a == 1 ? noy : noz;
     const double faca = a == 0 ? fac0 : a == 1 ? fac1 : fac2;
     const int m = dca < 0 ? -1 : 0;
-    const CT s0 = shape_point<ORDER, CT>((CT)ooa - (CT)m, i);
-    const CT ds = shape_point<ORDER, CT>((CT)noa + (CT)(dca - m), i) - s0;
+    CT s0, s1;
+    wpair<ORDER, CT>(ooa, noa, dca, m, i, s0, s1);
+    const CT ds = s1 - s0;
     const CT u = s0 + CT(0.5) * ds, v = CT(0.5) * s0 + ds * CT(1.0 / 3.0);
-    CT run = ds;
+    double run = (double)ds;   // exact, so the closing residue is too
 #pragma unroll
     for (int o = 1; o < NS; o <<= 1) {
-        const CT y = __shfl_up_sync(FULL, run, o);
+        const double y = __shfl_up_sync(FULL, run, o);
         if (i >= o) run += y;
     }
-    const CT P = (CT)(faca * (double)w) * run;
+    const CT P = (CT)(faca * (double)w * run);
     const int ntx = dcx ? NS : NS - 1, nty = dcy ? NS : NS - 1, ntz = dcz ? NS : NS - 1;
     const int ax = lx + min(dcx, 0), ay = ly + min(dcy, 0), az = lz + min(dcz, 0);
     F *base = jt + (az * jy + ay) * jx + ax;
@@ -364,10 +406,11 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
         const int dcc = c == 0 ? dcx : c == 1 ? dcy : dcz;
         const int nt1 = a1 == 0 ? ntx : a1 == 1 ? nty : ntz;
         const int nt2 = a2 == 0 ? ntx : a2 == 1 ? nty : ntz;
-        const int na = dcc ? NA : NA - 1;
+        const int na = dcc < 0 ? NA + 1 : NA;   // up to the reference's min(hi, NP - 2)
         const int per_a = nt1 * nt2, npts = na * per_a;
         // x / d for x < 2^10, d <= 64 (exact): multiply by ceil(2^16 / d)
         const unsigned r_pa = 65536u / per_a + 1u, r_n2 = 65536u / nt2 + 1u;
+        const int ehi = (PLUS || dcc <= 0) ? 1 : 0;   // window's top edge
         F *Jc = base + c * JV;
         for (int p0 = 0; p0 < npts; p0 += 32) {   // warp-uniform passes
             const int p = p0 + lane;
@@ -379,14 +422,14 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
             const CT s02 = __shfl_sync(FULL, s0, a2 * NS + j2);
             const CT ds2 = __shfl_sync(FULL, ds, a2 * NS + j2);
             const CT Pv = __shfl_sync(FULL, P, c * NS + ja);
-            // entries of the owner cell's register window (own-relative edge
-            // -1..0, points -1..1; anchor-relative index j <-> own-relative
-            // j - 1 + m) were already added by deposit_window
+            // entries of the owner cell's register window (anchor-relative
+            // index j <-> own-relative j - 1 + m) were already added by
+            // deposit_window
             const int mc = dcc < 0 ? -1 : 0;
             const int m1 = (a1 == 0 ? dcx : a1 == 1 ? dcy : dcz) < 0 ? -1 : 0;
             const int m2 = (a2 == 0 ? dcx : a2 == 1 ? dcy : dcz) < 0 ? -1 : 0;
             const int e = ja - 1 + mc, p1 = j1 - 1 + m1, p2 = j2 - 1 + m2;
-            const bool inside = e >= -1 && e <= 0 && p1 >= -1 && p1 <= 1 && p2 >= -1 && p2 <= 1;
+            const bool inside = e >= -1 && e <= ehi && p1 >= -1 && p1 <= 1 && p2 >= -1 && p2 <= 1;
             if (p < npts && !(skip_window && inside)) {
                 const CT T = u1 * s02 + v1 * ds2;
                 const CT val = Pv * T;
@@ -407,12 +450,15 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
 // footprint OUTSIDE the owner cell's register window (deposit_window adds
 // the rest in registers).  Axes are rotated so the crossing axis is A0; with
 // the anchor min(old, new) its supports span indices 1..4, the other axes
-// 1..3; the full footprint is
-//   J_A0: along 1..3 x (A1: 1..3) x (A2: 1..3)  = 27 entries
-//   J_A1: along 1..2 x (A0: 1..4) x (A2: 1..3)  = 24 entries
-//   J_A2: along 1..2 x (A0: 1..4) x (A1: 1..3)  = 24 entries
-// of which the window holds 18 + 18 + 18: this routine adds the other
-// 9 + 6 + 6 (one along-edge of J_A0, one A0 point of J_A1 / J_A2).
+// 1..3; the full footprint (pic/kernels.py:204-248, closing entries kept) is
+//   J_A0: along 1..3 (+k) / 0..3 (-k) x (A1: 1..3) x (A2: 1..3)
+//   J_A1: along 1..3 x (A0: 1..4) x (A2: 1..3)  = 36 entries
+//   J_A2: along 1..3 x (A0: 1..4) x (A1: 1..3)  = 36 entries
+// The float32 window holds own-relative edges -1..+1 x points -1..1, so this
+// adds J_A0's edge -2 (-k only) and the A0 point outside the window of
+// J_A1 / J_A2 (3 edges x 3): 18 (+k) or 27 (-k) CAS.  The float64 window
+// holds edge +1 only as the closing residue (dc <= 0), so for +k J_A0's
+// edge +1 (a real entry) comes here too.
 // (the transverse factor is symmetric in its two axes, so the reference's
 // per-component axis order does not matter).  TSC/CIC only.
 template <typename F, int ORDER>
@@ -421,36 +467,36 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
                                             F ooz, F nox, F noy, F noz, F w, double fac0,
                                             double fac1, double fac2) {
     using CT = F;
+    constexpr bool PLUS = sizeof(F) == 4;
     const int a1 = k == 2 ? 0 : k + 1, a2 = k == 0 ? 2 : k - 1;
     const F oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
     const double fac[3] = {fac0, fac1, fac2};
     const int st[3] = {1, jx, jx * jy};
     const int m = dck < 0 ? -1 : 0;
     CT s0c[4], dsc[4], s0p[3], dsp[3], s0q[3], dsq[3];
-    {
-        CT t0[Shape<ORDER>::NP - 1], t1[Shape<ORDER>::NP - 1];
-        shape_anchor<ORDER, CT>((CT)oo[k] - (CT)m, t0);
-        shape_anchor<ORDER, CT>((CT)no[k] + (CT)(dck - m), t1);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { s0c[i] = t0[i]; dsc[i] = t1[i] - t0[i]; }
-        shape_anchor<ORDER, CT>((CT)oo[a1], t0);
-        shape_anchor<ORDER, CT>((CT)no[a1], t1);
+    for (int i = 0; i < 4; ++i) {
+        CT t1;
+        wpair<ORDER, CT>(oo[k], no[k], dck, m, i, s0c[i], t1);
+        dsc[i] = t1 - s0c[i];
+    }
 #pragma unroll
-        for (int i = 0; i < 3; ++i) { s0p[i] = t0[i]; dsp[i] = t1[i] - t0[i]; }
-        shape_anchor<ORDER, CT>((CT)oo[a2], t0);
-        shape_anchor<ORDER, CT>((CT)no[a2], t1);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) { s0q[i] = t0[i]; dsq[i] = t1[i] - t0[i]; }
+    for (int i = 0; i < 3; ++i) {
+        CT t1;
+        wpair<ORDER, CT>(oo[a1], no[a1], 0, 0, i, s0p[i], t1);
+        dsp[i] = t1 - s0p[i];
+        wpair<ORDER, CT>(oo[a2], no[a2], 0, 0, i, s0q[i], t1);
+        dsq[i] = t1 - s0q[i];
     }
     const int lc[3] = {lx, ly, lz};
     F *base = jt + (lc[2] + (k == 2 ? m : 0)) * st[2] + (lc[1] + (k == 1 ? m : 0)) * st[1] +
               (lc[0] + (k == 0 ? m : 0));
     const int sk = st[k], s1_ = st[a1], s2_ = st[a2];
-    // J_k: along k (1..3) x a1 (1..3) x a2 (1..3)
-    {
+    // J_k: along k x a1 (1..3) x a2 (1..3), the edge outside the window:
+    // -k -> own edge -2 (anchor index 0); +k -> own edge +1 (float64 only)
+    if (!PLUS || m != 0) {
         F *J = base + k * JV;
         const CT fw = (CT)(fac[k] * (double)w);
-        // only the edge outside the owner's window: +k -> edge 3, -k -> edge 1
         const int ja = m == 0 ? 2 : 0;
         const CT Pout = m == 0 ? fw * ((dsc[0] + dsc[1]) + dsc[2]) : fw * dsc[0];
 #pragma unroll
@@ -463,7 +509,7 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
             }
         }
     }
-    // J_a1: along a1 (1..2) x k (1..4) x a2 (1..3);  J_a2: along a2 (1..2) x k x a1
+    // J_a1: along a1 (1..3) x k (1..4) x a2 (1..3);  J_a2: along a2 (1..3) x k x a1
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int c = h == 0 ? a1 : a2;
@@ -471,8 +517,11 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
         const CT *s0o = h == 0 ? s0q : s0p, *dso = h == 0 ? dsq : dsp;   // the other transverse
         const int sa = h == 0 ? s1_ : s2_, so = h == 0 ? s2_ : s1_;
         F *J = base + c * JV;
-        const CT fw = (CT)(fac[c] * (double)w);
+        const double fwd = fac[c] * (double)w;
+        const CT fw = (CT)fwd;
         const CT P0 = fw * dsa[0], P1 = fw * (dsa[0] + dsa[1]);
+        // the closing residue, from the exact sum
+        const CT P2 = (CT)(fwd * (((double)dsa[0] + (double)dsa[1]) + (double)dsa[2]));
         // only the point along k outside the owner's window: +k -> 4, -k -> 1
         const int j1 = m == 0 ? 3 : 0;
         const CT s0j = m == 0 ? s0c[3] : s0c[0], dsj = m == 0 ? dsc[3] : dsc[0];
@@ -483,113 +532,101 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
             F *p = J + (j1 + 1) * sk + (j2 + 1) * so;
             atomicAdd(p + sa, (F)(P0 * T));
             atomicAdd(p + 2 * sa, (F)(P1 * T));
+            atomicAdd(p + 3 * sa, (F)(P2 * T));
         }
     }
 }
 
-// Shape weights at support indices 1..3 of a particle with in-cell offset
-// x in [0, 1] (its whole CIC/TSC support), in fp32:
-//   TSC: 0.5 (1-x)^2, 0.75 - (x-1/2)^2, 0.5 x^2      (pic/kernels.py:138-150)
-//   CIC: max(1/2-x, 0), 1 - |x-1/2|, max(x-1/2, 0)
-template <int ORDER>
-__device__ __forceinline__ void shape123f(float x, float (&s)[3]) {
-    if (ORDER == 2) {
-        const float a = 1.0f - x, b = x - 0.5f;
-        s[0] = __fmul_rn(0.5f, __fmul_rn(a, a));
-        s[1] = __fmaf_rn(-b, b, 0.75f);
-        s[2] = __fmul_rn(0.5f, __fmul_rn(x, x));
-    } else {
-        s[0] = fmaxf(0.5f - x, 0.0f);
-        s[1] = 1.0f - fabsf(x - 0.5f);
-        s[2] = fmaxf(x - 0.5f, 0.0f);
-    }
-}
-
-// Old and new position of one axis at once (TSC: packed f32x2 arithmetic,
-// the same round-to-nearest operations as shape123f on each half).
-template <int ORDER>
-__device__ __forceinline__ void shape123f_pair(float xo, float xn, float (&so)[3], float (&sn)[3]) {
-    if (ORDER == 2) {
-        const float2 x = make_float2(xo, xn);
-        const float2 a = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-xo, -xn));
-        const float2 b = __fadd2_rn(x, make_float2(-0.5f, -0.5f));
-        const float2 h = make_float2(0.5f, 0.5f);
-        const float2 s0 = __fmul2_rn(h, __fmul2_rn(a, a));
-        const float2 s1 = __ffma2_rn(make_float2(-b.x, -b.y), b, make_float2(0.75f, 0.75f));
-        const float2 s2 = __fmul2_rn(h, __fmul2_rn(x, x));
-        so[0] = s0.x; so[1] = s1.x; so[2] = s2.x;
-        sn[0] = s0.y; sn[1] = s1.y; sn[2] = s2.y;
-    } else {
-        shape123f<ORDER>(xo, so);
-        shape123f<ORDER>(xn, sn);
-    }
-}
-
-// Register accumulation of a particle that stays in its cell (dc = 0):
-// J_a(ja, j1, j2) += P_ja * fw_a * T(j1, j2) for ja in {1, 2}, j1, j2 in
-// {1, 2, 3}, with P the running sum of ds along a and
+// The register window of the owner cell (every particle, crossing or not):
+// J accumulators at own-relative edges -1, 0, +1 along a component x points
+// -1..1 across it, in registers -- 81 per thread (float32).  Entry (edge e,
+// j1, j2) of component a gets P_e T(j1, j2): P_e = fw_a x the running sum
+// of ds_a from the reference's lo to point e (pic/kernels.py:204-222), and
 // T = (s0 + ds/2)_1 s0_2 + (s0/2 + ds/3)_1 ds_2 (the reference's transverse
-// factor, factorised).  The closing entry ja = 3 is sum(s1) - sum(s0), a
-// rounding residue, and is dropped.  fp32 with FMA: J is compared within
-// tolerance, never bitwise (the reference's own J order is not fixed).
-// The (ja = 1, ja = 2) pair of an entry shares T: one packed FFMA2
-// (__ffma2_rn, sm_100) updates both -- the same two round-to-nearest FMAs.
-#ifndef KWB_NO_FFMA2
+// factor :215-218, factorised), in fp32 with FMA -- J is compared within
+// tolerance (the reference's own J order is not fixed).  Edge +1 is the
+// closing entry sum(s1) - sum(s0) for dc_a <= 0 -- a rounding residue of
+// the F weights that the reference deposits, and at thermal speeds ~1e-6 of
+// J -- so its running sum is formed exactly in double.  A particle that
+// moved dc in {-1,0,1} on an axis has its new shape on points dc-1..dc+1:
+// the window sees it shifted (zero filled), and for dc = -1 the running sum
+// starts one point earlier (ds at point -2).  The entries of a crosser
+// outside the window go through the queue (deposit_cross1 / deposit_warp).
+// (edge -1, edge 0) of an entry share T: one packed FFMA2 (__ffma2_rn,
+// sm_100) updates both -- the same two round-to-nearest FMAs; edge +1 pairs
+// the j1 = 0, 1 entries.
 struct RegAcc {
-    float2 p[3][3][3];  // [component][j1-1][j2-1] = {ja=1, ja=2}
+    float2 p[3][3][3];  // [component][j1][j2] = {edge -1, edge 0}
+    float2 q[3][3];     // [component][j2] = edge +1 at {j1 = 0, j1 = 1}  (unused with
+    float r[3][3];      // [component][j2] = edge +1 at j1 = 2             KWB_WIN_SMEM)
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int b = 0; b < 3; ++b)
+            for (int b = 0; b < 3; ++b) {
 #pragma unroll
                 for (int d = 0; d < 3; ++d) p[c][b][d] = make_float2(0.f, 0.f);
+                q[c][b] = make_float2(0.f, 0.f);
+                r[c][b] = 0.f;
+            }
     }
-    __device__ __forceinline__ float get(int c, int a, int b, int d) const {
-        return a == 0 ? p[c][b][d].x : p[c][b][d].y;
+    // e: 0, 1, 2 = edge -1, 0, +1
+    __device__ __forceinline__ float get(int c, int e, int b, int d) const {
+        return e == 0 ? p[c][b][d].x
+             : e == 1 ? p[c][b][d].y
+             : (b == 0 ? q[c][d].x : b == 1 ? q[c][d].y : r[c][d]);
     }
     __device__ __forceinline__ static float2 pack(float lo, float hi) { return make_float2(lo, hi); }
     __device__ __forceinline__ void fma2(int c, int b, int d, float2 P, float T) {
         p[c][b][d] = __ffma2_rn(P, make_float2(T, T), p[c][b][d]);
     }
 };
-#else
-struct RegAcc {
-    float a[3][2][3][3];  // [component][ja-1][j1-1][j2-1]
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int a_ = 0; a_ < 2; ++a_)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) a[c][a_][b][d] = 0.f;
-    }
-    __device__ __forceinline__ float get(int c, int a_, int b, int d) const { return a[c][a_][b][d]; }
-};
-#endif
 
-// The window of every particle, crossing or not: the register accumulators
-// cover own-relative edges -1..0 along a component and points -1..1
-// transverse.  A particle that moved dc in {-1,0,1} on an axis has its new
-// shape on points dc-1..dc+1: the window sees it shifted (zero filled), and
-// for dc = -1 the along-axis running sum starts one point earlier (ds at
-// point -2).  For dc = 0 this is exactly the stayer deposit; the entries of
-// a crosser outside the window go through the queue (deposit_cross1 /
-// deposit_warp skip the window).
+// Per-thread shared-memory copy of the edge +1 accumulators (KWB_WIN_SMEM):
+// float4 k of thread t at ws[k * kMaxCells + t]; component c in float4s
+// 2c, 2c+1 (q[c][0..2], r[c][0..1]) and lane c of float4 6 (r[c][2]).
+__device__ __forceinline__ void win_load(const float4 *ws, float2 (&q)[3][3], float (&r)[3][3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float4 A = ws[(2 * c) * kMaxCells], B = ws[(2 * c + 1) * kMaxCells];
+        q[c][0] = make_float2(A.x, A.y); q[c][1] = make_float2(A.z, A.w);
+        q[c][2] = make_float2(B.x, B.y); r[c][0] = B.z; r[c][1] = B.w;
+    }
+    const float4 C = ws[6 * kMaxCells];
+    r[0][2] = C.x; r[1][2] = C.y; r[2][2] = C.z;
+}
+__device__ __forceinline__ void win_store(float4 *ws, const float2 (&q)[3][3], const float (&r)[3][3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        ws[(2 * c) * kMaxCells] = make_float4(q[c][0].x, q[c][0].y, q[c][1].x, q[c][1].y);
+        ws[(2 * c + 1) * kMaxCells] = make_float4(q[c][2].x, q[c][2].y, r[c][0], r[c][1]);
+    }
+    ws[6 * kMaxCells] = make_float4(r[0][2], r[1][2], r[2][2], 0.0f);
+}
+
 template <int ORDER>
-__device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, float ooz,
-                                             float nox, float noy, float noz, float fwx,
-                                             float fwy, float fwz, int dcx, int dcy, int dcz) {
-    float s0[3][3], ds[3][3], dm2[3];
+__device__ __forceinline__ void deposit_window(RegAcc &R, float4 *ws, float oox, float ooy,
+                                               float ooz, float nox, float noy, float noz,
+                                               float fwx, float fwy, float fwz, int dcx, int dcy,
+                                               int dcz) {
+#ifdef KWB_WIN_SMEM
+    float2 Q[3][3];
+    float Rr[3][3];
+    win_load(ws, Q, Rr);
+#else
+    float2 (&Q)[3][3] = R.q;
+    float (&Rr)[3][3] = R.r;
+#endif
+    float s0[3][3], ds[3][3], dm2[3], rs[3];
     {
         const float oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
         const int dc[3] = {dcx, dcy, dcz};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             float s1[3];
-            shape123f_pair<ORDER>(oo[a], no[a], s0[a], s1);
+            wref3<ORDER, float>((double)oo[a], 0.0, s0[a]);
+            const double c = (double)dc[a];
+            wref3<ORDER, float>(c + (double)no[a], c, s1);   // own points dc-1 .. dc+1
             const float w0 = dc[a] == 0 ? s1[0] : (dc[a] > 0 ? 0.0f : s1[1]);
             const float w1 = dc[a] == 0 ? s1[1] : (dc[a] > 0 ? s1[0] : s1[2]);
             const float w2 = dc[a] == 0 ? s1[2] : (dc[a] > 0 ? s1[1] : 0.0f);
@@ -597,6 +634,8 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
             ds[a][0] = __fsub_rn(w0, s0[a][0]);
             ds[a][1] = __fsub_rn(w1, s0[a][1]);
             ds[a][2] = __fsub_rn(w2, s0[a][2]);
+            rs[a] = (float)((((double)dm2[a] + (double)ds[a][0]) + (double)ds[a][1]) +
+                            (double)ds[a][2]);
         }
     }
     const float fw[3] = {fwx, fwy, fwz};
@@ -606,92 +645,74 @@ __device__ __forceinline__ void deposit_stay(RegAcc &R, float oox, float ooy, fl
         const float r1 = __fadd_rn(dm2[c], ds[c][0]);
         const float p1 = __fmul_rn(fw[c], r1);
         const float p2 = __fmul_rn(fw[c], __fadd_rn(r1, ds[c][1]));
-#ifndef KWB_NO_FFMA2
+        const float p3 = __fmul_rn(fw[c], rs[c]);
         const auto P12 = RegAcc::pack(p1, p2);
-#endif
-#ifndef KWB_NO_FFMA2
-        {   // T for j1 = 0, 1 as one f32x2 pair (same roundings), j1 = 2 scalar
-            const auto U01 = RegAcc::pack(__fmaf_rn(0.5f, ds[a1][0], s0[a1][0]),
-                                          __fmaf_rn(0.5f, ds[a1][1], s0[a1][1]));
-            const auto V01 = RegAcc::pack(
-                __fmaf_rn(1.0f / 3.0f, ds[a1][0], __fmul_rn(0.5f, s0[a1][0])),
-                __fmaf_rn(1.0f / 3.0f, ds[a1][1], __fmul_rn(0.5f, s0[a1][1])));
-            const float u2 = __fmaf_rn(0.5f, ds[a1][2], s0[a1][2]);
-            const float v2 = __fmaf_rn(1.0f / 3.0f, ds[a1][2], __fmul_rn(0.5f, s0[a1][2]));
+        const auto P33 = RegAcc::pack(p3, p3);
+        // T for j1 = 0, 1 as one f32x2 pair (same roundings), j1 = 2 scalar
+        const auto U01 = RegAcc::pack(__fmaf_rn(0.5f, ds[a1][0], s0[a1][0]),
+                                      __fmaf_rn(0.5f, ds[a1][1], s0[a1][1]));
+        const auto V01 = RegAcc::pack(
+            __fmaf_rn(1.0f / 3.0f, ds[a1][0], __fmul_rn(0.5f, s0[a1][0])),
+            __fmaf_rn(1.0f / 3.0f, ds[a1][1], __fmul_rn(0.5f, s0[a1][1])));
+        const float u2 = __fmaf_rn(0.5f, ds[a1][2], s0[a1][2]);
+        const float v2 = __fmaf_rn(1.0f / 3.0f, ds[a1][2], __fmul_rn(0.5f, s0[a1][2]));
 #pragma unroll
-            for (int j2 = 0; j2 < 3; ++j2) {
-                const float2 vd = __fmul2_rn(V01, make_float2(ds[a2][j2], ds[a2][j2]));
-                const float2 T01 = __ffma2_rn(U01, make_float2(s0[a2][j2], s0[a2][j2]), vd);
-                const float T0 = T01.x, T1 = T01.y;
-                R.fma2(c, 0, j2, P12, T0);
-                R.fma2(c, 1, j2, P12, T1);
-                R.fma2(c, 2, j2, P12, __fmaf_rn(u2, s0[a2][j2], __fmul_rn(v2, ds[a2][j2])));
-            }
+        for (int j2 = 0; j2 < 3; ++j2) {
+            const float2 vd = __fmul2_rn(V01, make_float2(ds[a2][j2], ds[a2][j2]));
+            const float2 T01 = __ffma2_rn(U01, make_float2(s0[a2][j2], s0[a2][j2]), vd);
+            const float T2 = __fmaf_rn(u2, s0[a2][j2], __fmul_rn(v2, ds[a2][j2]));
+            R.fma2(c, 0, j2, P12, T01.x);
+            R.fma2(c, 1, j2, P12, T01.y);
+            R.fma2(c, 2, j2, P12, T2);
+            Q[c][j2] = __ffma2_rn(P33, T01, Q[c][j2]);
+            Rr[c][j2] = __fmaf_rn(p3, T2, Rr[c][j2]);
         }
-#else
-#pragma unroll
-        for (int j1 = 0; j1 < 3; ++j1) {
-            const float u = __fmaf_rn(0.5f, ds[a1][j1], s0[a1][j1]);
-            const float v = __fmaf_rn(1.0f / 3.0f, ds[a1][j1], __fmul_rn(0.5f, s0[a1][j1]));
-#pragma unroll
-            for (int j2 = 0; j2 < 3; ++j2) {
-                const float T = __fmaf_rn(u, s0[a2][j2], __fmul_rn(v, ds[a2][j2]));
-                R.a[c][0][j1][j2] = __fmaf_rn(p1, T, R.a[c][0][j1][j2]);
-                R.a[c][1][j1][j2] = __fmaf_rn(p2, T, R.a[c][1][j1][j2]);
-            }
-        }
-#endif
     }
+#ifdef KWB_WIN_SMEM
+    win_store(ws, Q, Rr);
+#endif
 }
 
-// float64 storage: the same register deposit in double (108 registers of
-// accumulators, so these kernels run one CTA per SM); J in float64 is
-// compared at 1e-13 and the FMA-contracted sums stay far inside it.
+// float64 storage: the same window in double for edges -1 and 0 (108
+// registers of accumulators, so these kernels run one CTA per SM) plus the
+// closing residue of edge +1 (dc <= 0 only: for dc = +1 edge +1 is a real
+// entry and goes through the queue) in float -- it is ~1e-16 of J, so
+// float is far more than enough.  J in float64 is compared at 1e-13.
 struct RegAccD {
-    double a[3][2][3][3];  // [component][ja-1][j1-1][j2-1]
+    double a[3][2][3][3];  // [component][edge -1, 0][j1][j2]
+    float r[3][3][3];      // [component][j1][j2] closing residue at edge +1
     __device__ __forceinline__ void zero() {
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int a_ = 0; a_ < 2; ++a_)
+            for (int b = 0; b < 3; ++b)
 #pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) a[c][a_][b][d] = 0.0;
+                for (int d = 0; d < 3; ++d) {
+                    a[c][0][b][d] = 0.0;
+                    a[c][1][b][d] = 0.0;
+                    r[c][b][d] = 0.f;
+                }
     }
-    __device__ __forceinline__ double get(int c, int a_, int b, int d) const {
-        return a[c][a_][b][d];
+    __device__ __forceinline__ double get(int c, int e, int b, int d) const {
+        return e < 2 ? a[c][e][b][d] : (double)r[c][b][d];
     }
 };
 
 template <int ORDER>
-__device__ __forceinline__ void shape123d(double x, double (&s)[3]) {
-    if (ORDER == 2) {
-        const double a = 1.0 - x, b = x - 0.5;
-        s[0] = 0.5 * (a * a);
-        s[1] = __fma_rn(-b, b, 0.75);
-        s[2] = 0.5 * (x * x);
-    } else {
-        s[0] = fmax(0.5 - x, 0.0);
-        s[1] = 1.0 - fabs(x - 0.5);
-        s[2] = fmax(x - 0.5, 0.0);
-    }
-}
-
-template <int ORDER>
-__device__ __forceinline__ void deposit_stay_d(RegAccD &R, double oox, double ooy, double ooz,
-                                               double nox, double noy, double noz, double fwx,
-                                               double fwy, double fwz, int dcx, int dcy,
-                                               int dcz) {
-    double s0[3][3], ds[3][3], dm2[3];
+__device__ __forceinline__ void deposit_window_d(RegAccD &R, double oox, double ooy, double ooz,
+                                                 double nox, double noy, double noz, double fwx,
+                                                 double fwy, double fwz, int dcx, int dcy,
+                                                 int dcz) {
+    double s0[3][3], ds[3][3], dm2[3], rs[3];
     {
         const double oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
         const int dc[3] = {dcx, dcy, dcz};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             double s1[3];
-            shape123d<ORDER>(oo[a], s0[a]);
-            shape123d<ORDER>(no[a], s1);
+            wref3<ORDER, double>(oo[a], 0.0, s0[a]);
+            const double c = (double)dc[a];
+            wref3<ORDER, double>(c + no[a], c, s1);
             const double w0 = dc[a] == 0 ? s1[0] : (dc[a] > 0 ? 0.0 : s1[1]);
             const double w1 = dc[a] == 0 ? s1[1] : (dc[a] > 0 ? s1[0] : s1[2]);
             const double w2 = dc[a] == 0 ? s1[2] : (dc[a] > 0 ? s1[1] : 0.0);
@@ -699,6 +720,7 @@ __device__ __forceinline__ void deposit_stay_d(RegAccD &R, double oox, double oo
             ds[a][0] = w0 - s0[a][0];
             ds[a][1] = w1 - s0[a][1];
             ds[a][2] = w2 - s0[a][2];
+            rs[a] = dc[a] <= 0 ? ((dm2[a] + ds[a][0]) + ds[a][1]) + ds[a][2] : 0.0;
         }
     }
     const double fw[3] = {fwx, fwy, fwz};
@@ -708,6 +730,7 @@ __device__ __forceinline__ void deposit_stay_d(RegAccD &R, double oox, double oo
         const double r1 = dm2[c] + ds[c][0];
         const double p1 = fw[c] * r1;
         const double p2 = fw[c] * (r1 + ds[c][1]);
+        const float p3 = (float)(fw[c] * rs[c]);
 #pragma unroll
         for (int j1 = 0; j1 < 3; ++j1) {
             const double u = __fma_rn(0.5, ds[a1][j1], s0[a1][j1]);
@@ -717,6 +740,7 @@ __device__ __forceinline__ void deposit_stay_d(RegAccD &R, double oox, double oo
                 const double T = __fma_rn(u, s0[a2][j2], v * ds[a2][j2]);
                 R.a[c][0][j1][j2] = __fma_rn(p1, T, R.a[c][0][j1][j2]);
                 R.a[c][1][j1][j2] = __fma_rn(p2, T, R.a[c][1][j1][j2]);
+                R.r[c][j1][j2] = __fmaf_rn(p3, (float)T, R.r[c][j1][j2]);
             }
         }
     }
@@ -734,8 +758,9 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
 // One PCS stayer per lane into the warp's boxes (see kBoxX); every lane of
 // the warp calls this together (on = false: the lane adds nothing).  Same
 // density decomposition and factors as deposit_cross_compact with dc = 0
-// (pic/kernels.py:210-248, SURVEY.md §8c PCS).  (rx, ry) = cell relative to
-// the warp's 8 x 4 patch.
+// (pic/kernels.py:210-248, SURVEY.md §8c PCS), closing entries included.
+// (rx, ry) = cell relative to the warp's 8 x 4 patch.  Box layout: x
+// fastest, 12 x 8 x 5 per component at 0 / 480 / 960.
 // One group: all loads, then all stores (entries of a group never alias
 // across the warp's lanes), so the N read-add-writes overlap.
 template <int N>
@@ -751,11 +776,29 @@ __device__ __forceinline__ void box_group(float *b, int stride, const float (&v)
                      : "memory");
     __syncwarp();   // measured: without it lanes lose updates (tests/test_gpu_dense.py)
 }
+
+// PCS weights (the reference's recipe) at own points -2..2
+// of a particle at offset x in [0, 1]: the distances are x + 1.5, x + 0.5,
+// |x - 0.5|, 1.5 - x, 2.5 - x, so points 0 and +-2 need one branch each.
+__device__ __forceinline__ void wref5_pcs(double x, float (&s)[5]) {
+    auto outer = [](double d) {   // 1 <= d: (2 - d)^3 / 6, 0 from d = 2
+        const double e = 2.0 - d;
+        return d < 2.0 ? div6((e * e) * e) : 0.0;
+    };
+    auto inner = [](double d) { return div6((4.0 - (6.0 * d) * d) + ((3.0 * d) * d) * d); };
+    const double d0 = x + 1.5, d1 = x + 0.5, d2 = fabs(x - 0.5), d3 = 1.5 - x, d4 = 2.5 - x;
+    s[0] = (float)outer(d0);
+    s[1] = (float)(d1 < 1.0 ? inner(d1) : outer(d1));
+    s[2] = (float)inner(d2);
+    s[3] = (float)(d3 < 1.0 ? inner(d3) : outer(d3));
+    s[4] = (float)outer(d4);
+}
+
 __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx, int ry, bool on,
                                                 float oox, float ooy, float ooz, float nox,
                                                 float noy, float noz, float w, double fac0,
                                                 double fac1, double fac2) {
-    float s0[3][5], ds[3][5], P[3][4];
+    float s0[3][5], ds[3][5], P[3][5];
     {
         // an idle lane's records may be stale bit patterns: never let them
         // reach the arithmetic (0 * NaN would poison the box)
@@ -764,16 +807,17 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
         const double fac[3] = {fac0, fac1, fac2};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            float a0[6], a1[6];
-            shape_anchor<3, float>(oo[a], a0);
-            shape_anchor<3, float>(no[a], a1);
-            const float fw = on ? (float)(fac[a] * (double)w) : 0.0f;   // w read only when on
-            float run = 0.0f;
+            float a0[5], a1[5];
+            wref5_pcs((double)oo[a], a0);
+            wref5_pcs((double)no[a], a1);
+            const double fw = on ? fac[a] * (double)w : 0.0;   // w read only when on
+            double run = 0.0;
 #pragma unroll
             for (int i = 0; i < 5; ++i) {
                 s0[a][i] = a0[i];
                 ds[a][i] = a1[i] - a0[i];
-                if (i < 4) { run += ds[a][i]; P[a][i] = fw * run; }
+                run += (double)ds[a][i];
+                P[a][i] = (float)(fw * run);   // i = 4: the closing residue, exact
             }
         }
     }
@@ -783,23 +827,23 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
         float y0[5], y1[5];
 #pragma unroll
         for (int j = 0; j < 5; ++j) { y0[j] = s0[1][j]; y1[j] = ds[1][j]; }
-        float *b = box + rx + 11 * ry;
+        float *b = box + rx + 12 * ry;
 #pragma unroll 1
         for (int j1 = 0; j1 < 5; ++j1) {
             const float uu = y0[0] + 0.5f * y1[0], vv = 0.5f * y0[0] + y1[0] * (1.0f / 3.0f);
             float T[5];
 #pragma unroll
             for (int j2 = 0; j2 < 5; ++j2) T[j2] = uu * s0[2][j2] + vv * ds[2][j2];
-            float pa[4] = {P[0][0], P[0][1], P[0][2], P[0][3]};
+            float pa[5] = {P[0][0], P[0][1], P[0][2], P[0][3], P[0][4]};
 #pragma unroll 1
-            for (int ja = 0; ja < 4; ++ja) {
+            for (int ja = 0; ja < 5; ++ja) {
                 float v[5];
 #pragma unroll
                 for (int j2 = 0; j2 < 5; ++j2) v[j2] = pa[0] * T[j2];
-                box_group<5>(b + ja, 11 * 8, v);
-                pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3];
+                box_group<5>(b + ja, 96, v);
+                pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3]; pa[3] = pa[4];
             }
-            b += 11;
+            b += 12;
 #pragma unroll
             for (int j = 0; j < 4; ++j) { y0[j] = y0[j + 1]; y1[j] = y1[j + 1]; }
         }
@@ -814,20 +858,20 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
             vz[j] = 0.5f * s0[2][j] + ds[2][j] * (1.0f / 3.0f);
             x0[j] = s0[0][j]; x1[j] = ds[0][j];
         }
-        float *b = box + 440 + rx + 12 * ry;
+        float *b = box + 480 + rx + 12 * ry;
 #pragma unroll 1
         for (int j2 = 0; j2 < 5; ++j2) {
             float T[5];
 #pragma unroll
             for (int j1 = 0; j1 < 5; ++j1) T[j1] = uz[j1] * x0[0] + vz[j1] * x1[0];
-            float pa[4] = {P[1][0], P[1][1], P[1][2], P[1][3]};
+            float pa[5] = {P[1][0], P[1][1], P[1][2], P[1][3], P[1][4]};
 #pragma unroll 1
-            for (int ja = 0; ja < 4; ++ja) {
+            for (int ja = 0; ja < 5; ++ja) {
                 float v[5];
 #pragma unroll
                 for (int j1 = 0; j1 < 5; ++j1) v[j1] = pa[0] * T[j1];
-                box_group<5>(b + 12 * ja, 12 * 7, v);
-                pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3];
+                box_group<5>(b + 12 * ja, 96, v);
+                pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3]; pa[3] = pa[4];
             }
             b += 1;
 #pragma unroll
@@ -843,7 +887,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
             ux[j] = s0[0][j] + 0.5f * ds[0][j];
             vx[j] = 0.5f * s0[0][j] + ds[0][j] * (1.0f / 3.0f);
         }
-        float *b = box + 860 + rx + 12 * ry;
+        float *b = box + 960 + rx + 12 * ry;
 #pragma unroll 1
         for (int j1 = 0; j1 < 5; ++j1) {
             const float uu = ux[0], vv = vx[0];
@@ -853,10 +897,10 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
 #pragma unroll 1
             for (int j2 = 0; j2 < 5; ++j2) {
                 const float T = uu * y0[0] + vv * y1[0];
-                float v[4];
+                float v[5];
 #pragma unroll
-                for (int ja = 0; ja < 4; ++ja) v[ja] = P[2][ja] * T;
-                box_group<4>(b + 12 * j2, 12 * 8, v);
+                for (int ja = 0; ja < 5; ++ja) v[ja] = P[2][ja] * T;
+                box_group<5>(b + 12 * j2, 96, v);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) { y0[j] = y0[j + 1]; y1[j] = y1[j + 1]; }
             }
@@ -986,6 +1030,12 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
     std::conditional_t<sizeof(F) == 4, RegAcc, RegAccD> R;
     if (REGACC) R.zero();
+    float4 *wsm = reinterpret_cast<float4 *>(smem_raw + L.off_ws) + t;   // KWB_WIN_SMEM
+#ifdef KWB_WIN_SMEM
+    if (REGACC && sizeof(F) == 4 && owner)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) wsm[k * kMaxCells] = make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
     const double qm = sp.qm_half_dt;
     const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
     const double cxd = (double)cx, cyd = (double)cy, czd = (double)cz;
@@ -1163,12 +1213,12 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 // crosser deposits outside it goes through the queue
                 const double ww = (double)w;
                 if constexpr (sizeof(F) == 4)
-                    deposit_stay<ORDER>(R, (float)ox, (float)oy, (float)oz, (float)nox,
+                    deposit_window<ORDER>(R, wsm, (float)ox, (float)oy, (float)oz, (float)nox,
                                         (float)noy, (float)noz, (float)(sp.fac[0] * ww),
                                         (float)(sp.fac[1] * ww), (float)(sp.fac[2] * ww),
                                         dcx, dcy, dcz);
                 else
-                    deposit_stay_d<ORDER>(R, (double)ox, (double)oy, (double)oz, (double)nox,
+                    deposit_window_d<ORDER>(R, (double)ox, (double)oy, (double)oz, (double)nox,
                                           (double)noy, (double)noz, sp.fac[0] * ww,
                                           sp.fac[1] * ww, sp.fac[2] * ww, dcx, dcy, dcz);
 #ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
@@ -1254,12 +1304,15 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     // ---- reduce the register accumulators into the J tile ----------------
     // Sweep s adds accumulator s of every cell: the targets cell + offset(s)
     // are distinct across threads, so plain read-modify-writes are race free;
-    // the three components go to different arrays and share a sweep (18
-    // sweeps); the barrier orders consecutive sweeps.
+    // the three components go to different arrays and share a sweep (27
+    // sweeps: edges -1, 0, +1 x 3 x 3); the barrier orders consecutive sweeps.
     if (REGACC) {
         F *Jb = jt + ((lz * L.jy) + ly) * L.jx + lx;
+#ifdef KWB_WIN_SMEM
+        if constexpr (sizeof(F) == 4) win_load(wsm, R.q, R.r);
+#endif
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int b = 0; b < 3; ++b)
 #pragma unroll
@@ -1285,16 +1338,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         for (int e = lane; e < kBoxFloats; e += 32) {
             const float v = wbox[e];
             if (v != 0.0f) {
-                int c, X, Y, Z;
-                if (e < 440) {
-                    c = 0; X = e % 11; Y = (e / 11) % 8; Z = e / 88;
-                } else if (e < 860) {
-                    const int r = e - 440;
-                    c = 1; X = r % 12; Y = (r / 12) % 7; Z = r / 84;
-                } else {
-                    const int r = e - 860;
-                    c = 2; X = r % 12; Y = (r / 12) % 8; Z = r / 96;
-                }
+                const int c = e / 480, r = e - c * 480;
+                const int X = r % 12, Y = (r / 12) % 8, Z = r / 96;
                 atomicAdd(jt + c * L.JV + ((Z + z0 + 1) * L.jy + (Y + y0 + 1)) * L.jx + (X + 1), v);
             }
         }

@@ -61,6 +61,68 @@ CASES = {
 }
 
 
+# BASELINE-scale cases (SURVEY.md §8c golden plan): C1 in full (32^3, 8 ppc,
+# electrons, thermal 0.05, TSC, 100 steps) in fp64 and fp32, and 32^3
+# proxies of C2-C4 with their ppc, species and distribution (10 steps).
+# Stored as SHA-256 digests of every lattice and every packed particle array
+# at each dumped step (they pin the oracle bitwise at scale,
+# tests/test_oracle_golden.py), per-cell occupancy and per-super-cell counts
+# at each dump, diagnostics, and -- for C1 -- the nine lattices at the last
+# step (the GPU free-running test compares against the reference's own).
+BIG = {
+    "c1_tsc_f64": dict(cells=(32, 32, 32), ppc=8, species="e", dtype="float64",
+                       stream_velocity=0.0, perturbation=0.0, thermal_u=0.05,
+                       seed=1, steps=(0, 1, 10, 100), fields_at=(100,)),
+    "c1_tsc_f32": dict(cells=(32, 32, 32), ppc=8, species="e", dtype="float32",
+                       stream_velocity=0.0, perturbation=0.0, thermal_u=0.05,
+                       seed=1, steps=(0, 1, 10, 100), fields_at=(100,)),
+    "c2p_f32": dict(cells=(32, 32, 32), ppc=25, species="pair", mass_ratio=1836.0,
+                    dtype="float32", stream_velocity=0.0, perturbation=0.0, thermal_u=0.05,
+                    seed=2, steps=(0, 1, 10), fields_at=()),
+    "c3p_f32": dict(cells=(32, 32, 32), ppc=16, species="pair", mass_ratio=1.0,
+                    dtype="float32", stream_velocity=0.2, perturbation=0.01, thermal_u=0.01,
+                    seed=3, steps=(0, 1, 10), fields_at=()),
+    "c4p_f32": dict(cells=(32, 32, 32), ppc=32, species="e", dtype="float32",
+                    stream_velocity=0.0, perturbation=0.0, thermal_u=0.05,
+                    seed=4, steps=(0, 1, 10), fields_at=()),
+}
+
+
+def run_big(name, c):
+    import time
+    params = make_params(c)
+    t0 = time.time()
+    sim = init_khi(params, seed=c["seed"], backend=SerialBackend(), validate=True)
+    out = {}
+    meta = {"case": name, "config": {k: v for k, v in c.items() if k != "fields_at"},
+            "dt": params.dt, "steps": {}, "digests": True}
+    last = max(c["steps"])
+    for t in range(last + 1):
+        if t in c["steps"]:
+            key = f"t{t}"
+            f = sim.fields
+            sm = {"residual": sim.last_residual, "diagnostics": sim.diagnostics(),
+                  "census": sim.census(), "species": [],
+                  "fields": {n: digest(getattr(f, n)) for n in kwf.ALL_COMPONENTS}}
+            for i, st in enumerate(sim.stores):
+                pk = st.packed()
+                sm["species"].append({k: digest(v) for k, v in pk.items()})
+                out[f"{key}_s{i}_sc_counts"] = sc_counts(st)
+                out[f"{key}_s{i}_occupancy"] = occupancy(st, params.cells.as_tuple()).astype(np.int16)
+            if t in c["fields_at"]:
+                for n in kwf.ALL_COMPONENTS:
+                    out[f"{key}_{n}"] = getattr(f, n).copy()
+            meta["steps"][key] = sm
+        if t < last:
+            sim.step()
+    meta["reference_seconds"] = time.time() - t0
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+    with open(os.path.join(OUT, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print(name, "census", sim.census(), "residual", sim.last_residual,
+          f"{meta['reference_seconds']:.1f} s", flush=True)
+
+
 def make_params(c):
     if c["species"] == "e":
         sp = (Species("electron", -1.0, 1.0, 1.0 / c["ppc"]),)
@@ -143,7 +205,11 @@ def kat():
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(CASES)
+    names = sys.argv[1:] or list(CASES) + list(BIG)
     for n in names:
-        run_case(n, CASES[n])
-    kat()
+        if n in BIG:
+            run_big(n, BIG[n])
+        else:
+            run_case(n, CASES[n])
+    if not sys.argv[1:]:
+        kat()

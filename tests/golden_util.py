@@ -51,3 +51,8 @@ def rel_l2(a, b) -> float:
     nb = np.linalg.norm(b)
     d = np.linalg.norm(a - b)
     return float(d / nb) if nb > 0 else float(d)
+
+
+# BASELINE-scale cases (tests/golden/make_golden.py BIG): digests at every
+# dumped step, occupancy and super-cell counts, C1 lattices at t = 100.
+BIG_CASES = ("c1_tsc_f64", "c1_tsc_f32", "c2p_f32", "c3p_f32", "c4p_f32")

@@ -72,43 +72,78 @@ def make_pair(meta, shape="tsc", validate=True):
     return gpu, orc
 
 
-def shadow_error(orc, steps=1):
-    """Intrinsic rounding error of the storage-precision reference for the
-    current state: relative L2 between the oracle stepped in its own dtype and
-    a float64 shadow stepped from the same (exactly widened) state.  Used to
-    state the field tolerance for f32 cases whose J is a cancellation of
-    species currents (e.g. KHI pairs), where the reference itself is only
-    accurate to ~1e-5.  Does not advance `orc`."""
-    import copy
+def record(case, name, err, tol, kind="1step", spread=0.0):
+    """Append one measured relative-L2 error to $KWB_PARITY_LOG (JSON lines)
+    so a GPU run leaves the per-case parity table behind
+    (tools/parity_table.py -> profiles/r02_parity.md)."""
+    import json
+    import os
+    path = os.environ.get("KWB_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps({"case": case, "field": name, "err": float(err),
+                                 "tol": float(tol), "kind": kind,
+                                 "spread": float(spread)}) + "\n")
+
+
+def order_spread(orc, steps=1, variants=((1, False), (0, True), (2, True))):
+    """The reference's own J spread on the current oracle state: relative L2
+    between the oracle in the Serial back-end's order (bit for bit the
+    reference) and the same step in other valid accumulation orders -- tiles
+    merged in a BlockPool-like random order (kw/backends.py:115-139, worker
+    completion order) and/or each frame's particles walked backwards (the
+    reference's particle order within a super cell is an accident of its
+    migration history, pic/particles.py:238-287).  f32 J is a sum of
+    hundreds of rounded contributions per entry, so its value depends on that
+    order: ~2e-7 for C1-like thermal plasma, ~1e-6 for dense hot plasma and
+    ~1e-5 where the species currents cancel (KHI pairs) -- the stated f32
+    bar 1e-6 (calibrated on the merge order alone) is below
+    the reference's own order noise there.  Max over `variants` of (merge
+    seed, reversed slots); does not advance `orc`."""
     from oracle.pic import OracleSim
-    if orc.dtype == np.float64:
-        return {n: 0.0 for n in FIELDS9}
-    p32 = orc.params
-    a = OracleSim(p32, validate=False, shape_order=orc.shape_order)
-    import dataclasses
-    if dataclasses.is_dataclass(p32):   # SimParams is frozen
-        p64 = dataclasses.replace(p32, dtype=np.dtype(np.float64))
-    else:
-        p64 = copy.copy(p32)
-        p64.dtype = np.dtype(np.float64)
-    b = OracleSim(p64, validate=False, shape_order=orc.shape_order)
-    for so, sa, sb in zip(orc.stores, a.stores, b.stores):
-        pk = so.packed()
-        scx, scy, scz = so.super_cell
-        gx, gy, _ = so.sc_grid
-        sc = (pk["cx"] // scx) + gx * ((pk["cy"] // scy) + gy * (pk["cz"] // scz))
-        sa.load_packed(sc, pk)
-        sb.load_packed(sc, {k: (v.astype(np.float64) if v.dtype.kind == "f" else v)
-                            for k, v in pk.items()})
-    for n in FIELDS9:
-        setattr(a.fields, n, getattr(orc.fields, n).copy())
-        setattr(b.fields, n, getattr(orc.fields, n).astype(np.float64))
-    a.run(steps)
-    b.run(steps)
-    return {n: rel_l2(getattr(a.fields, n), getattr(b.fields, n)) for n in FIELDS9}
+
+    def clone(seed, rev):
+        a = OracleSim(orc.params, validate=False, shape_order=orc.shape_order,
+                      threads=orc.threads)
+        a.merge_seed = seed
+        a.reverse_slots = rev
+        for so, sa in zip(orc.stores, a.stores):
+            pk = so.packed()
+            scx, scy, scz = so.super_cell
+            gx, gy, _ = so.sc_grid
+            sc = (pk["cx"] // scx) + gx * ((pk["cy"] // scy) + gy * (pk["cz"] // scz))
+            sa.load_packed(sc, pk)
+        for n in FIELDS9:
+            setattr(a.fields, n, getattr(orc.fields, n).copy())
+        a.run(steps)
+        return a
+
+    base = clone(0, False)
+    worst = {n: 0.0 for n in FIELDS9}
+    for sd, rev in variants:
+        b = clone(sd, rev)
+        for n in FIELDS9:
+            worst[n] = max(worst[n], rel_l2(getattr(b.fields, n), getattr(base.fields, n)))
+    return worst
 
 
-def field_tol(base, shadow, n):
-    """Tolerance for lattice n: the stated bar, or 3x the reference's own
-    intrinsic error when that is larger (ill-conditioned J)."""
-    return max(base, 3.0 * shadow.get(n, 0.0))
+SPREAD_FACTOR = 3.0
+
+
+def check_fields(case, gpu_fields, ref_get, tol, names=FIELDS9, kind="1step", spread=None):
+    """Relative L2 of every lattice against the reference, each within `tol`
+    -- or within SPREAD_FACTOR x the reference's own order spread on this
+    state when `spread` (order_spread) is given and larger -- recorded for
+    the parity table."""
+    errs = {}
+    bad = {}
+    for n in names:
+        err = rel_l2(gpu_fields.numpy(n), ref_get(n))
+        sp = spread.get(n, 0.0) if spread else 0.0
+        t = max(tol, SPREAD_FACTOR * sp)
+        record(case, n, err, t, kind, sp)
+        errs[n] = err
+        if not err <= t:
+            bad[n] = (err, t)
+    assert not bad, (case, bad)
+    return errs

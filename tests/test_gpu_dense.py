@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from golden_util import rel_l2
-from parity_util import TOL_1STEP, TOL_RESID, assert_particles_bitwise
+from parity_util import TOL_1STEP, TOL_RESID, assert_particles_bitwise, check_fields, order_spread
 
 pytestmark = pytest.mark.gpu
 
@@ -33,11 +33,11 @@ def test_dense_hot_plasma_one_step(shape):
             gpu.load_state(fields={n: getattr(orc.fields, n) for n in
                                    ("Ex", "Ey", "Ez", "Bx", "By", "Bz", "Jx", "Jy", "Jz")},
                            particles=[st.packed() for st in orc.stores])
+        spread = order_spread(orc)
         gpu.step()
         orc.step()
         for gs, os_ in zip(gpu.stores, orc.stores):
             assert_particles_bitwise(gs, os_)
-        for n in ("Jx", "Jy", "Jz"):
-            err = rel_l2(gpu.fields.numpy(n), getattr(orc.fields, n))
-            assert err <= TOL_1STEP[np.dtype(np.float32)] * 10, (n, err)
+        check_fields(f"dense_{shape}:step{it}", gpu.fields, lambda n: getattr(orc.fields, n),
+                     TOL_1STEP[np.dtype(np.float32)], names=("Jx", "Jy", "Jz"), spread=spread)
         assert gpu.last_residual <= TOL_RESID[np.dtype(np.float32)]

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 from golden_util import rel_l2
-from parity_util import FIELDS9, assert_particles_bitwise
+from parity_util import FIELDS9, TOL_1STEP, assert_particles_bitwise
 
 pytestmark = pytest.mark.gpu
 
@@ -44,7 +44,7 @@ def _load(p, gpu, orc, records):
 
 def _step_and_compare(p, gpu, orc, steps=2, tol=None):
     dt = np.dtype(p.dtype)
-    tol = tol or (1e-12 if dt == np.float64 else 1e-5)
+    tol = tol or TOL_1STEP[dt]
     for t in range(steps):
         if t:
             gpu.load_state(fields={n: getattr(orc.fields, n) for n in FIELDS9},
@@ -167,7 +167,7 @@ def test_graph_replay_matches_direct_launches(dtype):
     a.use_graphs, b.use_graphs = True, False
     a.enqueue_step()
     b.enqueue_step()
-    tol = 1e-5 if dtype == np.float32 else 1e-12
+    tol = TOL_1STEP[np.dtype(dtype)]
     for t in range(4):
         b.load_state(fields={n: a.fields.numpy(n) for n in FIELDS9},
                      particles=[st.packed() for st in a.stores])
@@ -265,7 +265,7 @@ def test_zslab_entry_identity_plane_table_matches_advance(dtype, shape):
     J3 = ("Jx", "Jy", "Jz")
     b._jplanes = torch.tensor([b.fields.storage(n)[z].data_ptr() for n in J3 for z in range(nz)],
                               dtype=torch.int64, device=b.device)
-    tol = 1e-5 if dtype == np.float32 else 1e-12
+    tol = TOL_1STEP[np.dtype(dtype)]
     for t in range(2):
         # teacher forced: the J atomics' summation order differs between
         # runs, so each step starts b from a's state

@@ -15,8 +15,8 @@ import torch
 
 from golden_util import CASES, load_case, oracle_params, rel_l2
 from parity_util import (FIELDS9, TOL_1STEP, TOL_FREE, TOL_GAUSS, TOL_RESID,
-                         assert_particles_bitwise, field_tol, gpu_params, make_pair,
-                         occupancy, shadow_error)
+                         assert_particles_bitwise, check_fields, order_spread, gpu_params, make_pair,
+                         occupancy, record)
 
 pytestmark = pytest.mark.gpu
 
@@ -58,15 +58,13 @@ def test_one_step_vs_oracle(name):
     gpu, orc = make_pair(meta)
     for gs, os_ in zip(gpu.stores, orc.stores):
         assert_particles_bitwise(gs, os_)            # identical initial state
-    shadow = shadow_error(orc)
+    spread = order_spread(orc)
     gpu.step()
     orc.step()
     for gs, os_ in zip(gpu.stores, orc.stores):
         assert_particles_bitwise(gs, os_)
-    tol = TOL_1STEP[_dtype(meta)]
-    for n in FIELDS9:
-        err = rel_l2(gpu.fields.numpy(n), getattr(orc.fields, n))
-        assert err <= field_tol(tol, shadow, n), (n, err, shadow[n])
+    check_fields(f"{name}:init", gpu.fields, lambda n: getattr(orc.fields, n),
+                 TOL_1STEP[_dtype(meta)], spread=spread)
     assert gpu.last_residual <= TOL_RESID[_dtype(meta)]
 
 
@@ -81,15 +79,13 @@ def test_teacher_forced_from_evolved_state(name):
                    particles=[st.packed() for st in orc.stores])
     for gs, os_ in zip(gpu.stores, orc.stores):
         assert_particles_bitwise(gs, os_)
-    shadow = shadow_error(orc)
+    spread = order_spread(orc)
     gpu.step()
     orc.step()
     for gs, os_ in zip(gpu.stores, orc.stores):
         assert_particles_bitwise(gs, os_)
-    tol = TOL_1STEP[_dtype(meta)]
-    for n in FIELDS9:
-        err = rel_l2(gpu.fields.numpy(n), getattr(orc.fields, n))
-        assert err <= field_tol(tol * 10, shadow, n), (n, err, shadow[n])
+    check_fields(f"{name}:evolved3", gpu.fields, lambda n: getattr(orc.fields, n),
+                 TOL_1STEP[_dtype(meta)], spread=spread)
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -111,9 +107,8 @@ def test_free_running_vs_reference_golden(name):
                 ref = data[f"{key}_s{i}_occupancy"].astype(np.int64)
                 displaced = int(np.abs(occ - ref).sum()) // 2
                 assert displaced <= (0 if dt == np.float64 else 4), (key, i, displaced)
-            for n in FIELDS9:
-                err = rel_l2(sim.fields.numpy(n), data[f"{key}_{n}"])
-                assert err <= TOL_FREE[dt], (key, n, err)
+            check_fields(f"{name}:free:{key}", sim.fields, lambda n: data[f"{key}_{n}"],
+                         TOL_FREE[dt], kind="free")
             if t > 0:
                 assert sim.last_residual <= TOL_RESID[dt]
                 assert sim.last_gauss_drift <= TOL_GAUSS[dt]
@@ -139,14 +134,13 @@ def test_extended_shapes_vs_oracle(shape, name):
         if it:
             gpu.load_state(fields={n: getattr(orc.fields, n) for n in FIELDS9},
                            particles=[st.packed() for st in orc.stores])
-        shadow = shadow_error(orc)
+        spread = order_spread(orc)
         gpu.step()
         orc.step()
         for gs, os_ in zip(gpu.stores, orc.stores):
             assert_particles_bitwise(gs, os_)
-        for n in ("Jx", "Jy", "Jz"):
-            err = rel_l2(gpu.fields.numpy(n), getattr(orc.fields, n))
-            assert err <= field_tol(TOL_1STEP[dt] * 10, shadow, n), (n, err)
+        check_fields(f"{name}:{shape}:step{it}", gpu.fields, lambda n: getattr(orc.fields, n),
+                     TOL_1STEP[dt], spread=spread)
         assert gpu.last_residual <= TOL_RESID[dt]
         assert orc.last_residual <= TOL_RESID[dt]
         if it == 0:

@@ -1,0 +1,170 @@
+"""Parity at BASELINE scale (SURVEY.md §8c golden plan).
+
+* C1 in full -- 32^3 cells, 8 ppc electrons, thermal_u 0.05, TSC, fp64 and
+  fp32 -- free-running 100 steps from init_khi against the unmodified
+  reference (tests/golden/c1_tsc_*.{json,npz}, made by make_golden.py; the
+  oracle run alongside reproduces the reference's digests bit for bit,
+  tests/test_oracle_golden.py): census and per-super-cell counts exact at
+  every dump, per-cell occupancy exact (fp64) / <= 4 particles displaced
+  (fp32), fields within 1e-12 / 1e-4 (t = 100 against the reference's own
+  lattices), continuity residual and Gauss drift within the bars EVERY
+  step.
+* 32^3 proxies of C2 (25 ppc e/ion 1836), C3 (16 ppc KHI pair) and C4
+  (32 ppc electrons; TSC and the CIC/PCS extension) teacher-forced from
+  the oracle's state after 10 steps: particle records bitwise, fields within
+  1e-6 (fp32) -- or 3x the reference's own accumulation-order spread on
+  that state (parity_util.order_spread) where that is larger.
+* A C5-shaped z-slab decomposition (G = 2 slabs through the loopback
+  transport, fused and unfused J halo) against the oracle of the global
+  problem: teacher-forced one step, and 10 free-running steps.
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import load_case, oracle_params, rel_l2
+from parity_util import (FIELDS9, TOL_1STEP, TOL_FREE, TOL_GAUSS, TOL_RESID,
+                         assert_particles_bitwise, check_fields, gpu_params, occupancy,
+                         order_spread, sorted_records)
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(meta, shape="tsc", validate=True):
+    from oracle.pic import oracle_init_khi
+    from paper_1606_02862_b200.pic import init_khi
+    op = oracle_params(meta)
+    order = {"cic": 1, "tsc": 2, "pcs": 3}[shape]
+    seed = meta["config"]["seed"]
+    gpu = init_khi(gpu_params(op, shape), seed=seed, validate=validate)
+    orc = oracle_init_khi(op, seed=seed, validate=validate, shape_order=order)
+    return gpu, orc
+
+
+@pytest.mark.parametrize("name", ["c1_tsc_f64", "c1_tsc_f32"])
+def test_c1_free_running_100_steps(name):
+    meta, data = load_case(name)
+    dt = np.dtype(meta["config"]["dtype"])
+    gpu, orc = _pair(meta)
+    cells = tuple(meta["config"]["cells"])
+    steps = sorted(int(k[1:]) for k in meta["steps"])
+    worst_resid = worst_gauss = 0.0
+    for t in range(max(steps) + 1):
+        if t in steps:
+            key = f"t{t}"
+            sm = meta["steps"][key]
+            assert gpu.census() == sm["census"] == orc.census()
+            for i, st in enumerate(gpu.stores):
+                np.testing.assert_array_equal(st.super_cell_counts(), data[f"{key}_s{i}_sc_counts"],
+                                              err_msg=key)
+                occ = occupancy(st.packed(), cells)
+                ref = data[f"{key}_s{i}_occupancy"].astype(np.int64)
+                displaced = int(np.abs(occ - ref).sum()) // 2
+                assert displaced <= (0 if dt == np.float64 else 4), (key, displaced)
+            if f"{key}_Ex" in data.files:   # the reference's own lattices
+                check_fields(f"{name}:free:{key}:reference", gpu.fields,
+                             lambda n: data[f"{key}_{n}"], TOL_FREE[dt], kind="free")
+            check_fields(f"{name}:free:{key}", gpu.fields, lambda n: getattr(orc.fields, n),
+                         TOL_FREE[dt], kind="free")
+            if t > 0:
+                d, ref_d = gpu.diagnostics(), sm["diagnostics"]
+                assert d["total_charge"] == pytest.approx(ref_d["total_charge"], rel=1e-9, abs=1e-9)
+                assert d["kinetic_energy"] == pytest.approx(ref_d["kinetic_energy"],
+                                                            rel=1e-12 if dt == np.float64 else 1e-6)
+        if t < max(steps):
+            gpu.step()
+            orc.step()
+            assert gpu.last_residual <= TOL_RESID[dt], (t, gpu.last_residual)
+            assert gpu.last_gauss_drift <= TOL_GAUSS[dt], (t, gpu.last_gauss_drift)
+            worst_resid = max(worst_resid, gpu.last_residual)
+            worst_gauss = max(worst_gauss, gpu.last_gauss_drift)
+    from parity_util import record
+    record(f"{name}:free:max_residual", "resid", worst_resid, TOL_RESID[dt], "free")
+    record(f"{name}:free:max_gauss_drift", "gauss", worst_gauss, TOL_GAUSS[dt], "free")
+
+
+@pytest.mark.parametrize("name,shape", [("c2p_f32", "tsc"), ("c3p_f32", "tsc"), ("c4p_f32", "tsc"),
+                                        ("c4p_f32", "cic"), ("c4p_f32", "pcs")])
+def test_proxy_teacher_forced_from_step_10(name, shape):
+    meta, _ = load_case(name)
+    dt = np.dtype(meta["config"]["dtype"])
+    gpu, orc = _pair(meta, shape=shape, validate=False)
+    orc.run(10)
+    gpu.load_state(fields={n: getattr(orc.fields, n) for n in FIELDS9},
+                   particles=[st.packed() for st in orc.stores])
+    for gs, os_ in zip(gpu.stores, orc.stores):
+        assert_particles_bitwise(gs, os_)
+    spread = order_spread(orc)
+    gpu.step()
+    orc.step()
+    for gs, os_ in zip(gpu.stores, orc.stores):
+        assert_particles_bitwise(gs, os_)
+    check_fields(f"{name}:{shape}:evolved10", gpu.fields, lambda n: getattr(orc.fields, n),
+                 TOL_1STEP[dt], spread=spread)
+
+
+def _c5_problem():
+    """C5's species and distribution (16 ppc electrons, thermal 0.05, TSC,
+    fp32) on a 32 x 32 x 32 global grid, z-decomposed into G = 2 slabs of 16
+    planes (4 super-cell layers each)."""
+    from types import SimpleNamespace as S
+    return S(cells=(32, 32, 32), dx=1.0, dy=1.0, dz=1.0, dt=0.95 / np.sqrt(3.0),
+             species=(S(name="electron", charge=-1.0, mass=1.0, weight=1.0 / 16),),
+             particles_per_cell=16, super_cell=(8, 8, 4), dtype=np.dtype(np.float32),
+             stream_velocity=0.0, perturbation=0.0, thermal_u=0.05)
+
+
+def _dec_from(orc, p, fuse_j):
+    from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
+    dec = DecomposedSimulation(p, 2, range(2), LoopbackTransport(), fuse_j=fuse_j)
+    dec.load_global(fields={n: getattr(orc.fields, n) for n in FIELDS9},
+                    particles=[st.packed() for st in orc.stores])
+    dec.refresh_guards()
+    return dec
+
+
+def _dec_particles(dec, i):
+    return {k: np.concatenate([dec.owned_particles(r, i)[k] for r in range(2)])
+            for k in ("cx", "cy", "cz", "ox", "oy", "oz", "ux", "uy", "uz", "w")}
+
+
+def _dec_field(dec, n):
+    return np.concatenate([dec.owned_fields(r, n) for r in range(2)], axis=2)
+
+
+@pytest.mark.parametrize("fuse_j", [True, False])
+def test_c5_shaped_decomposition_vs_oracle(fuse_j):
+    from oracle.pic import oracle_init_khi
+    op = _c5_problem()
+    p = gpu_params(op)
+    orc = oracle_init_khi(op, seed=5, validate=False)
+    # free-running 10 steps from the initial state
+    dec = _dec_from(orc, p, fuse_j)
+    ref = oracle_init_khi(op, seed=5, validate=False)
+    n0 = ref.census()
+    for t in range(10):
+        dec.step()
+        ref.step()
+        assert dec.census() == n0
+    occ = occupancy(_dec_particles(dec, 0), op.cells)
+    want = occupancy(ref.stores[0].packed(), op.cells)
+    assert int(np.abs(occ - want).sum()) // 2 <= 4
+    for n in FIELDS9:
+        err = rel_l2(_dec_field(dec, n), getattr(ref.fields, n))
+        assert err <= TOL_FREE[np.dtype(np.float32)], (n, err)
+    # teacher forced: one step from the oracle's evolved state
+    dec = _dec_from(ref, p, fuse_j)
+    spread = order_spread(ref)
+    dec.step()
+    ref.step()
+    a = sorted_records(_dec_particles(dec, 0))
+    b = sorted_records(ref.stores[0].packed())
+    for k in a:
+        np.testing.assert_array_equal(a[k].view(np.uint8), b[k].view(np.uint8), err_msg=k)
+
+    class _F:
+        @staticmethod
+        def numpy(n):
+            return _dec_field(dec, n)
+    check_fields(f"c5p_G2_{'fused' if fuse_j else 'nccl_path'}:evolved10", _F, lambda n: getattr(ref.fields, n),
+                 TOL_1STEP[np.dtype(np.float32)], spread=spread)

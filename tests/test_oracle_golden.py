@@ -82,3 +82,36 @@ def test_shared_reciprocal_division_is_ieee_division():
     fma, the same IEEE operation as __fma_rn)."""
     from oracle import pic as orc
     assert orc.lib().orc_div_rcp_check(1 << 24, 12345) == 0
+    # the PCS weights' a / 6 through the same construction (csrc/advance.cuh div6)
+    assert orc.lib().orc_div6_check(1 << 24, 777) == 0
+
+
+@pytest.mark.parametrize("name", ["c1_tsc_f64", "c1_tsc_f32", "c2p_f32", "c3p_f32", "c4p_f32"])
+def test_oracle_matches_reference_at_baseline_scale(name, oracle_lib):
+    """BASELINE scale: C1 in full (32^3 x 8 ppc, 100 steps) in fp64 and fp32
+    and 32^3 proxies of C2 (25 ppc e/ion 1836), C3 (16 ppc KHI pair) and C4
+    (32 ppc electrons), 10 steps.  The oracle reproduces the reference's
+    digests of every lattice and every packed particle array at each dumped
+    step bit for bit, plus occupancy, super-cell counts, the continuity
+    residual and diagnostics -- so the GPU tests may compare against the
+    oracle at these sizes (tests/test_gpu_scale.py)."""
+    meta, data = load_case(name)
+    p = oracle_params(meta)
+    sim = oracle_lib.oracle_init_khi(p, seed=meta["config"]["seed"], validate=True)
+    steps = sorted(int(k[1:]) for k in meta["steps"])
+    for t in range(max(steps) + 1):
+        if t in steps:
+            key = f"t{t}"
+            sm = meta["steps"][key]
+            assert sim.census() == sm["census"]
+            for i, st in enumerate(sim.stores):
+                pk = st.packed()
+                for k, v in pk.items():
+                    assert digest(v) == sm["species"][i][k], (key, i, k)
+                np.testing.assert_array_equal(st.super_cell_counts(), data[f"{key}_s{i}_sc_counts"])
+            for n in FIELDS9:
+                assert digest(getattr(sim.fields, n)) == sm["fields"][n], (key, n)
+            if t > 0:
+                assert sim.last_residual == sm["residual"]
+        if t < max(steps):
+            sim.step()
