@@ -55,12 +55,24 @@ def test_c1_free_running_100_steps(name):
             sm = meta["steps"][key]
             assert gpu.census() == sm["census"] == orc.census()
             for i, st in enumerate(gpu.stores):
-                np.testing.assert_array_equal(st.super_cell_counts(), data[f"{key}_s{i}_sc_counts"],
-                                              err_msg=key)
                 occ = occupancy(st.packed(), cells)
                 ref = data[f"{key}_s{i}_occupancy"].astype(np.int64)
                 displaced = int(np.abs(occ - ref).sum()) // 2
-                assert displaced <= (0 if dt == np.float64 else 4), (key, displaced)
+                # fp64: occupancy and super-cell counts exact.  fp32: <= 4
+                # particles displaced (the reference's own fp32 Serial vs
+                # BlockPool: 1 at step 100); a displaced
+                # particle may sit across a super-cell face, so the counts
+                # may differ by exactly the displaced particles and no more
+                dsc = np.abs(st.super_cell_counts().astype(np.int64)
+                             - data[f"{key}_s{i}_sc_counts"].astype(np.int64))
+                from parity_util import record
+                record(f"{name}:free:{key}:occupancy", "displaced", displaced,
+                       0 if dt == np.float64 else 4, "free")
+                if dt == np.float64:
+                    assert displaced == 0 and int(dsc.sum()) == 0, (key, displaced, int(dsc.sum()))
+                else:
+                    assert displaced <= 4 and int(dsc.sum()) // 2 <= displaced, \
+                        (key, displaced, int(dsc.sum()))
             if f"{key}_Ex" in data.files:   # the reference's own lattices
                 check_fields(f"{name}:free:{key}:reference", gpu.fields,
                              lambda n: data[f"{key}_{n}"], TOL_FREE[dt], kind="free")
