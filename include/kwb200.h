@@ -11,6 +11,7 @@
  *   kwb_particles_shift    <- migrate_particles   pic/particles.py:316-345
  *   kwb_fields_faraday_half<- FaradayHalfKernel   pic/kernels.py:415-431
  *   kwb_fields_ampere      <- AmpereKernel        pic/kernels.py:434-450
+ *   kwb_fields_gather      <- gather_fields       pic/fields.py:95-118
  *   kwb_charge_density     <- Simulation.charge_density / _rho_tsc
  *                             pic/sim.py:183-189, pic/kernels.py:291-326
  *   kwb_continuity_residual<- the validate block  pic/sim.py:168-175
@@ -159,6 +160,26 @@ int kwb_fields_faraday_half(const kwb_grid *g, void *const E[3], void *const B[3
                             double half_dt, kwb_stream_t stream);
 int kwb_fields_ampere(const kwb_grid *g, void *const E[3], void *const B[3],
                       void *const J[3], double dt, kwb_stream_t stream);
+
+/* Multi-GPU plumbing for the fused z-slab halo (pic/decomp.py): enable
+ * access from the CURRENT device to peer_device (already enabled = OK), and
+ * an asynchronous copy on the caller's stream (unified addressing; used for
+ * the E/B guard-plane pulls from the neighbour's lattices). */
+int kwb_enable_peer_access(int32_t peer_device);
+int kwb_copy_async(void *dst, const void *src, int64_t bytes, kwb_stream_t stream);
+
+/* Start of a step: J = 0 (J may be NULL to skip) and n_status status words
+ * = 0, in one kernel (pic/sim.py:138-140). */
+int kwb_zero_step(const kwb_grid *g, void *const J[3], int32_t *status, int32_t n_status,
+                  kwb_stream_t stream);
+
+/* E and B at n points (global cells[3n], in-cell offsets[3n] as double),
+ * out[6n] in the storage type: Ex Ey Ez Bx By Bz per point.  The advance
+ * kernel's gather recipe (pic/kernels.py:26-77).  Replaces the reference's
+ * host helper gather_fields (pic/fields.py:95-118). */
+int kwb_fields_gather(const kwb_grid *g, void *const E[3], void *const B[3], int64_t n,
+                      const int32_t *cells, const double *offsets, void *out,
+                      kwb_stream_t stream);
 
 /* Validation charge density (float64, accumulated, caller zeroes rho). */
 int kwb_charge_density(const kwb_grid *g, const kwb_species *sp, const kwb_store *st,

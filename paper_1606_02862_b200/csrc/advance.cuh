@@ -84,20 +84,6 @@ struct AdvCfg {
         sizeof(F) == 4 ? (ORDER == 3 ? KWB_MIN_BLOCKS_PCS : KWB_MIN_BLOCKS) : 1;
 };
 
-// a / b correctly rounded from r = RN(1 / b) (one IEEE division): q0 =
-// RN(a r) is within 1 ulp of a / b, the residual a - b q0 is exact with an
-// FMA, and RN(q0 + r (a - b q0)) is the correctly rounded quotient
-// (Markstein's theorem) -- so the push's and the move's three quotients by
-// one divisor (gamma, 1 + t^2, gamma') cost one division each, bit for bit
-// the reference's a / b.  An exact q0 is returned as is (the FMA would turn
-// -0 into +0).  The theorem needs no overflow or subnormal intermediates:
-// the operands are O(1) momenta and fields over divisors >= 1.
-__device__ __forceinline__ double div_rcp(double a, double b, double r) {
-    const double q0 = a * r;
-    const double e = __fma_rn(-q0, b, a);
-    return e == 0.0 ? q0 : __fma_rn(e, r, q0);   // e == 0: q0 exact, keeps -0 / b = -0
-}
-
 // a / 6 correctly rounded (the PCS weights' division) by
 // div_rcp with r = RN(1/6): three fp64 operations instead of a division.
 __device__ __forceinline__ double div6(double a) {

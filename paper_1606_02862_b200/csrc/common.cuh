@@ -20,6 +20,22 @@ __host__ __device__ __forceinline__ int pymod(int a, int n) {
     return r < 0 ? r + n : r;
 }
 
+// a / b correctly rounded from r = RN(1 / b) (one IEEE division): q0 =
+// RN(a r) is within 1 ulp of a / b, the residual a - b q0 is exact with an
+// FMA, and RN(q0 + r (a - b q0)) is the correctly rounded quotient
+// (Markstein's theorem) -- so the push's and the move's three quotients by
+// one divisor (gamma, 1 + t^2, gamma') cost one division each, and the Yee
+// updates' quotients by the cell sizes none, bit for bit the reference's
+// a / b (checked against IEEE division over 2^24 kernel-like pairs in the
+// CPU suite, oracle orc_div_rcp_check).  An exact q0 is returned as is (the
+// FMA would turn -0 into +0).  The theorem needs no overflow or subnormal
+// intermediates: the operands are O(1) momenta, fields and cell sizes.
+__device__ __forceinline__ double div_rcp(double a, double b, double r) {
+    const double q0 = a * r;
+    const double e = __fma_rn(-q0, b, a);
+    return e == 0.0 ? q0 : __fma_rn(e, r, q0);   // e == 0: q0 exact, keeps -0 / b = -0
+}
+
 // Field index for the x-fastest layout: (k * ny + j) * nx + i.
 __device__ __forceinline__ int64_t fidx(int i, int j, int k, int nx, int ny) {
     return ((int64_t)k * ny + j) * nx + i;

@@ -37,7 +37,7 @@ import numpy as np
 import torch
 
 from .. import _lib
-from ..errors import AllocationError
+from ..errors import AllocationError, ContractViolation
 from .params import SimParams
 
 E3 = ("Ex", "Ey", "Ez")
@@ -259,19 +259,30 @@ class DecomposedSimulation:
         if self._ipc:
             # every rank exports its 9-lattice field buffer; the J planes of
             # the z-neighbours are then plain device pointers in this process
+            import os
+
             from torch.multiprocessing.reductions import reduce_tensor
             (r,) = self.layouts
+            # an IPC handle is reopened on the PRODUCER's device index, so
+            # every rank must number the GPUs alike
+            vis = self.transport.all_gather_object(os.environ.get("CUDA_VISIBLE_DEVICES"))
+            if len(set(vis)) != 1:
+                raise ValueError("fuse_j across processes needs the same CUDA_VISIBLE_DEVICES on "
+                                 f"every rank (got {vis}): IPC handles carry device indices")
             handles = self.transport.all_gather_object(reduce_tensor(bufs[r]))
             mine = bufs[r].device
             for o in {self.layouts[r].lower, self.layouts[r].upper} - {r}:
                 fn, args = handles[o]
                 bufs[o] = fn(*args)
                 if bufs[o].device != mine:
-                    # the advance kernel red.adds into the peer's J from this
-                    # device: a cross-device copy makes torch enable peer
-                    # access mine -> peer (cudaDeviceEnablePeerAccess)
-                    torch.empty(1, dtype=bufs[o].dtype, device=mine).copy_(
-                        bufs[o].view(-1)[:1])
+                    # the advance kernel red.adds into the peer's J and the
+                    # guard pulls read the peer's planes FROM this device:
+                    # enable access mine -> peer explicitly
+                    if not torch.cuda.can_device_access_peer(mine, bufs[o].device):
+                        raise RuntimeError(f"fuse_j: {mine} cannot access {bufs[o].device} "
+                                           "(no peer path)")
+                    with torch.cuda.device(mine):
+                        _lib.call("kwb_enable_peer_access", int(bufs[o].device.index))
         self._fbufs = bufs              # field buffers of this slab and its neighbours
         for r, lay in self.layouts.items():
             owners = j_plane_owners(lay)
@@ -359,19 +370,9 @@ class DecomposedSimulation:
         detected right away (one flag all-reduced per step) and the exchange
         redone with larger messages.  checked=False (enqueue_step): no host
         synchronisation at all; an overflow surfaces in check_status()."""
-        if self.fuse_j:
-            for sim in self.locals.values():
-                sim.fields.zero_current()
-            if self._ipc:   # every neighbour's J is zero before anyone deposits
-                self.transport.device_barrier(next(iter(self.locals.values())).device)
         for sim in self.locals.values():
             sim._drain_status(keep=1)
-            if self.fuse_j:
-                sim.advance_particles(zero_j=False)
-            else:
-                sim.advance_particles()
-        if self._ipc:       # every deposit into this slab's J has landed
-            self.transport.device_barrier(next(iter(self.locals.values())).device)
+        self._advance_all(checked)
         if not self.fuse_j:
             self._exchange_j()
         self._exchange_particles(checked)
@@ -386,6 +387,52 @@ class DecomposedSimulation:
             sim.step_count += 1
             sim._post_status()
         self.step_count += 1
+
+    def _advance_all(self, checked):
+        """Every slab's particle phase.  checked=True gives the reference's
+        synchronous semantics (pic/kernels.py:405-408) across the slabs:
+        right after the advance -- before any exchange or field update --
+        every slab's status words are read and the flags all-reduced; a
+        particle that moved a full cell raises ContractViolation, and a full
+        cell column or exchange buffer undoes the phase on EVERY slab (the
+        input columns are intact: the advance is double-buffered; with the
+        fused halo the deposits already landed in the neighbours' J, which
+        is why all slabs zero J and redo together) and redoes it with grown
+        capacity."""
+        dev = next(iter(self.locals.values())).device
+        for _attempt in range(6):
+            if self.fuse_j:
+                for sim in self.locals.values():
+                    sim.fields.zero_current()
+                if self._ipc:   # every neighbour's J is zero before anyone deposits
+                    self.transport.device_barrier(dev)
+            for sim in self.locals.values():
+                if self.fuse_j:
+                    sim.advance_particles(zero_j=False)
+                else:
+                    sim.advance_particles()
+            if self._ipc:       # every deposit into this slab's J has landed
+                self.transport.device_barrier(dev)
+            if not checked or not all(hasattr(s_, "_read_status") for s_ in self.locals.values()):
+                return          # (host oracle slabs raise synchronously themselves)
+            sts = {r: sim._read_status() for r, sim in self.locals.items()}
+            flags = torch.zeros(2, dtype=torch.float64)
+            for st in sts.values():
+                flags[0] += float(st[:, _lib.ST_MOVE_ERRORS].sum())
+                flags[1] += float(st[:, _lib.ST_EXCH_OVERFLOW].sum()
+                                  + st[:, _lib.ST_STORE_OVERFLOW].sum())
+            if isinstance(self.transport, DistTransport):
+                t = flags.to(dev)
+                self.transport.all_reduce(t)
+                flags = t.cpu()
+            if flags[0] > 0:
+                raise ContractViolation(
+                    f"{int(flags[0])} particle(s) moved a full cell or more before deposit")
+            if flags[1] == 0:
+                return
+            for r, sim in self.locals.items():
+                sim._undo_particles(sts[r])
+        raise AllocationError("particle phase keeps overflowing its capacity")
 
     def enqueue_step(self):
         self.step(checked=False)
@@ -437,7 +484,10 @@ class DecomposedSimulation:
         p = self.params
         return {"total_charge": float(tot[0]), "kinetic_energy": float(tot[1]),
                 "field_energy": 0.5 * float(tot[2]) * p.dx * p.dy * p.dz,
-                "max_div_b": float(tot[3]), "max_continuity_residual": 0.0}
+                "max_div_b": float(tot[3]),
+                # the slabs run validate=False: no residual was computed, and a
+                # gate on it must not pass -- NaN compares false
+                "max_continuity_residual": float("nan")}
 
     def census(self) -> int:
         n = sum(s.census() for s in self.locals.values())
@@ -674,10 +724,19 @@ class DecomposedSimulation:
         for r, lay in self.layouts.items():
             dst = self._fbufs[r]
             gp, nzl = lay.gp, lay.nzl
+            stream = torch.cuda.current_stream(dst.device).cuda_stream
+            plane = dst[0, 0].numel() * dst.element_size()
+
+            def pull(dz, src, sz):
+                # one copy per contiguous lattice plane, on THIS slab's stream
+                # (a torch cross-device copy_ would run on the peer's stream)
+                for c in range(lo, hi):
+                    _lib.call("kwb_copy_async", dst[c, dz].data_ptr(), src[c, sz].data_ptr(),
+                              plane, stream)
             if "top" in sides:       # upper neighbour's first owned plane
-                dst[lo:hi, gp + nzl].copy_(self._fbufs[lay.upper][lo:hi, gp])
+                pull(gp + nzl, self._fbufs[lay.upper], gp)
             if "bottom" in sides:    # lower neighbour's last owned plane
-                dst[lo:hi, gp - 1].copy_(self._fbufs[lay.lower][lo:hi, gp + nzl - 1])
+                pull(gp - 1, self._fbufs[lay.lower], gp + nzl - 1)
 
     def _exchange_e_top(self):
         if self.fuse_j:

@@ -80,7 +80,13 @@ class YeeFieldSet:
         self._storage[name].copy_(a.permute(2, 1, 0).to(self.device))
 
     def zero_current(self) -> None:
-        self._buf[6:9].zero_()
+        """J = 0 on the current stream (kwb_zero_step)."""
+        import ctypes
+
+        from .. import _lib
+        _lib.call("kwb_zero_step", ctypes.byref(_grid_of(self)),
+                  ctypes.cast(_ptr3(self, J_COMPONENTS), ctypes.c_void_p), None, 0,
+                  torch.cuda.current_stream(self.device).cuda_stream)
 
 
 def _component_property(name):
@@ -135,6 +141,78 @@ def field_energy(fields: YeeFieldSet) -> float:
     from .sim import field_stats
     s, _ = field_stats(fields)
     return 0.5 * s * fields.dx * fields.dy * fields.dz
+
+
+def _grid_of(fields: YeeFieldSet):
+    from .. import _lib
+    g = _lib.Grid()
+    g.nx, g.ny, g.nz = fields.cells.as_tuple()
+    g.scx = g.scy = g.scz = 1
+    g.gx, g.gy, g.gz = g.nx, g.ny, g.nz
+    g.dtype = _lib.KWB_F32 if fields.dtype == np.float32 else _lib.KWB_F64
+    g.dx, g.dy, g.dz, g.dt = fields.dx, fields.dy, fields.dz, 0.0
+    return g
+
+
+def _ptr3(fields, names):
+    from .. import _lib
+    return _lib.ptr3([fields.storage(n) for n in names])
+
+
+def yee_update_b(fields: YeeFieldSet, half_dt: float) -> None:
+    """B <- B - half_dt * curl E (pic/fields.py:127-133) on the device, by
+    the same kernel as Simulation's Faraday half step (kwb_fields_faraday_half,
+    the compiled reference recipe pic/kernels.py:253-269 -- bit for bit the
+    reference's float64 result; in float32 the reference's whole-grid numpy
+    helper rounds differently and the kernel recipe is the one step() uses).
+    Asynchronous on the current stream."""
+    import ctypes
+
+    from .. import _lib
+    _lib.call("kwb_fields_faraday_half", ctypes.byref(_grid_of(fields)),
+              _ptr3(fields, E_COMPONENTS), _ptr3(fields, B_COMPONENTS), float(half_dt),
+              torch.cuda.current_stream(fields.device).cuda_stream)
+
+
+def yee_update_e(fields: YeeFieldSet, dt: float) -> None:
+    """E <- E + dt * (curl B - J) (pic/fields.py:136-142) on the device
+    (kwb_fields_ampere, pic/kernels.py:272-288).  Asynchronous."""
+    import ctypes
+
+    from .. import _lib
+    _lib.call("kwb_fields_ampere", ctypes.byref(_grid_of(fields)),
+              _ptr3(fields, E_COMPONENTS), _ptr3(fields, B_COMPONENTS),
+              _ptr3(fields, J_COMPONENTS), float(dt),
+              torch.cuda.current_stream(fields.device).cuda_stream)
+
+
+def gather_fields(fields: YeeFieldSet, p):
+    """(E, B) at a particle (pic/fields.py:95-118): trilinear interpolation of
+    the Yee-staggered lattices, evaluated on the device by kwb_fields_gather
+    with the advance kernel's recipe (double arithmetic, periodic wrap,
+    rounded to the storage type -- the values the reference's compiled
+    gather hands its push, pic/kernels.py:53-77).  ``p`` is a MacroParticle
+    (returns two length-3 arrays) or a sequence of them (returns (n, 3)
+    arrays).  Synchronises to return host arrays."""
+    import ctypes
+
+    from .. import _lib
+    single = hasattr(p, "cell")
+    ps = [p] if single else list(p)
+    n = len(ps)
+    cells = torch.tensor([list(q.cell) for q in ps] or [[0, 0, 0]], dtype=torch.int32,
+                         device=fields.device)
+    offs = torch.tensor([list(q.offset) for q in ps] or [[0.0, 0.0, 0.0]], dtype=torch.float64,
+                        device=fields.device)
+    out = torch.empty((max(n, 1), 6), dtype=fields.storage("Ex").dtype, device=fields.device)
+    _lib.call("kwb_fields_gather", ctypes.byref(_grid_of(fields)),
+              _ptr3(fields, E_COMPONENTS), _ptr3(fields, B_COMPONENTS), ctypes.c_int64(n),
+              _lib.ptr(cells), _lib.ptr(offs), _lib.ptr(out),
+              torch.cuda.current_stream(fields.device).cuda_stream)
+    h = out[:n].cpu().numpy()
+    if single:
+        return h[0, :3].copy(), h[0, 3:].copy()
+    return h[:, :3].copy(), h[:, 3:].copy()
 
 
 def yee_dispersion_omega(k: float, delta: float, dt: float) -> float:

@@ -55,6 +55,24 @@ def _near_cubic_factors(n: int) -> tuple[int, int, int]:
     return best
 
 
+class _nvtx:
+    """NVTX range around one stage of the cycle (visible in nsys / ncu
+    --nvtx): advance, shift, fields, validate.  Host-side only; a range
+    inside a CUDA-graph capture costs nothing at replay."""
+
+    __slots__ = ("name",)
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        torch.cuda.nvtx.range_pop()
+        return False
+
+
 def _grid_struct(p: SimParams) -> _lib.Grid:
     g = _lib.Grid()
     g.nx, g.ny, g.nz = p.cells.as_tuple()
@@ -289,26 +307,27 @@ class Simulation:
         slabs' deposits land in this slab's J before its own advance)."""
         stream = self._stream()
         g = ctypes.byref(self._grid)
-        if zero_j:
-            self.fields.zero_current()
-        self._status.zero_()
         E, B, J = self._E(), self._B(), self._J()
+        _lib.call("kwb_zero_step", g, ctypes.cast(J, ctypes.c_void_p) if zero_j else None,
+                  self._status.data_ptr(), self._status.numel(), stream)
         ex = self._exchange_buffer()
         jpl = getattr(self, "_jplanes", None)
         for i, st in enumerate(self.stores):
             src, dst = st.current, st.spare()
-            if jpl is None:
-                _lib.call("kwb_particles_advance", g, ctypes.byref(self._species[i]),
-                          ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
-                          ctypes.byref(ex.cstruct), E, B, J, self.shape_order,
-                          self._status[i].data_ptr(), stream)
-            else:
-                _lib.call("kwb_particles_advance_zslab", g, ctypes.byref(self._species[i]),
-                          ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
-                          ctypes.byref(ex.cstruct), E, B, J, jpl.data_ptr(),
-                          self.shape_order, self._status[i].data_ptr(), stream)
-            _lib.call("kwb_particles_shift", g, ctypes.byref(dst.cstruct()),
-                      ctypes.byref(ex.cstruct), self._status[i].data_ptr(), stream)
+            with _nvtx(f"advance[{i}]"):
+                if jpl is None:
+                    _lib.call("kwb_particles_advance", g, ctypes.byref(self._species[i]),
+                              ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
+                              ctypes.byref(ex.cstruct), E, B, J, self.shape_order,
+                              self._status[i].data_ptr(), stream)
+                else:
+                    _lib.call("kwb_particles_advance_zslab", g, ctypes.byref(self._species[i]),
+                              ctypes.byref(src.cstruct()), ctypes.byref(dst.cstruct()),
+                              ctypes.byref(ex.cstruct), E, B, J, jpl.data_ptr(),
+                              self.shape_order, self._status[i].data_ptr(), stream)
+            with _nvtx(f"shift[{i}]"):
+                _lib.call("kwb_particles_shift", g, ctypes.byref(dst.cstruct()),
+                          ctypes.byref(ex.cstruct), self._status[i].data_ptr(), stream)
             st.swap()
 
     def _undo_particles(self, st):
@@ -322,7 +341,8 @@ class Simulation:
             self._exchange = _Exchange(cap, self.stores[0].tdtype, self.device)
 
     def _enqueue_fields(self):
-        self.update_fields()
+        with _nvtx("fields"):
+            self.update_fields()
         if self.validate:
             g, stream = ctypes.byref(self._grid), self._stream()
             rho_new = self._charge_density_storage()

@@ -126,3 +126,25 @@ def test_guard_exchange_overflow_raises_when_unchecked():
         for _ in range(3):
             dec.enqueue_step()
         dec.check_status()
+
+
+def test_decomposed_checked_step_raises_before_field_update():
+    """checked step (the reference's synchronous semantics across slabs): a
+    particle that moves a full cell raises ContractViolation right after
+    the advance, before any exchange or field update (E and B untouched)."""
+    from paper_1606_02862_b200.errors import ContractViolation
+    from paper_1606_02862_b200.pic import SimParams, Species
+    from paper_1606_02862_b200.pic.decomp import DecomposedSimulation, LoopbackTransport
+    p = SimParams(cells=(16, 16, 24), species=(Species("e", -1.0, 1.0, 1.0),), dtype=np.float64)
+    dec = DecomposedSimulation(p, 2, range(2), LoopbackTransport())
+    pk = dict(cx=np.array([3, 5]), cy=np.array([3, 5]), cz=np.array([1, 14]),
+              ox=np.array([0.5, 3.0]), oy=np.array([0.5, 0.5]), oz=np.array([0.5, 0.5]),
+              ux=np.zeros(2), uy=np.zeros(2), uz=np.zeros(2), w=np.ones(2))
+    ex = np.full((16, 16, 24), 0.125)
+    dec.load_global(fields={"Ex": ex}, particles=[pk])
+    dec.refresh_guards()
+    with pytest.raises(ContractViolation, match="1 particle"):
+        dec.step()
+    got = np.concatenate([dec.owned_fields(r, "Ex") for r in range(2)], axis=2)
+    np.testing.assert_array_equal(got, ex)
+    assert np.isnan(dec.diagnostics()["max_continuity_residual"])

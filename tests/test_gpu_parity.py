@@ -242,3 +242,62 @@ def test_c2_shape_properties_at_64cubed():
     for st in sim.stores:
         assert st.check_integrity()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_field_helpers_gather_and_yee(dtype):
+    """Module helpers of the reference's pic/fields.py: yee_update_b /
+    yee_update_e equal the oracle's Faraday / Ampere bit for bit, and
+    gather_fields equals the reference's trilinear recipe (pic/kernels.py
+    :26-47, double arithmetic, rounded to the storage type) at random
+    points, bit for bit."""
+    from oracle.pic import OracleFields, lib as olib
+    import ctypes
+    from paper_1606_02862_b200.pic import (MacroParticle, STAGGER, YeeFieldSet, gather_fields,
+                                           yee_update_b, yee_update_e)
+    cells = (12, 10, 8)
+    deltas = (0.7, 1.0, 1.3)
+    f = YeeFieldSet(cells, *deltas, dtype=dtype)
+    of = OracleFields(cells, *deltas, dtype)
+    rng = np.random.default_rng(17)
+    for n in FIELDS9:
+        a = rng.standard_normal(cells).astype(dtype)
+        setattr(of, n, a)
+        f.load_numpy(n, a)
+    dt = 0.4
+    yee_update_b(f, dt / 2.0)
+    yee_update_e(f, dt)
+    cf = of._cfields()
+    sfx = "_f32" if np.dtype(dtype) == np.float32 else "_f64"
+    getattr(olib(), "orc_faraday" + sfx)(ctypes.byref(cf), dt / 2.0, 2)
+    getattr(olib(), "orc_ampere" + sfx)(ctypes.byref(cf), dt, 2)
+    for n in FIELDS9:
+        np.testing.assert_array_equal(f.numpy(n), getattr(of, n), err_msg=n)
+
+    def sample(a, px, py, pz, s):
+        nx, ny, nz = a.shape
+        tx, ty, tz = px - s[0], py - s[1], pz - s[2]
+        ix, iy, iz = int(np.floor(tx)), int(np.floor(ty)), int(np.floor(tz))
+        fx, fy, fz = tx - ix, ty - iy, tz - iz
+        A = lambda i, j, k: float(a[i % nx, j % ny, k % nz])
+        c00 = A(ix, iy, iz) * (1.0 - fx) + A(ix + 1, iy, iz) * fx
+        c10 = A(ix, iy + 1, iz) * (1.0 - fx) + A(ix + 1, iy + 1, iz) * fx
+        c01 = A(ix, iy, iz + 1) * (1.0 - fx) + A(ix + 1, iy, iz + 1) * fx
+        c11 = A(ix, iy + 1, iz + 1) * (1.0 - fx) + A(ix + 1, iy + 1, iz + 1) * fx
+        return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz
+
+    ps = [MacroParticle((int(rng.integers(0, cells[0])), int(rng.integers(0, cells[1])),
+                         int(rng.integers(0, cells[2]))),
+                        tuple(float(np.asarray(x, dtype=dtype)) for x in rng.random(3)),
+                        (0.0, 0.0, 0.0)) for _ in range(200)]
+    ps.append(MacroParticle((0, 0, 0), (0.0, 1.0, 0.5), (0.0, 0.0, 0.0)))
+    e, b = gather_fields(f, ps)
+    for q, p in enumerate(ps):
+        px, py, pz = (p.cell[a] + p.offset[a] for a in range(3))
+        want = [np.asarray(sample(f.numpy(n), px, py, pz, STAGGER[n]), dtype=dtype)
+                for n in ("Ex", "Ey", "Ez", "Bx", "By", "Bz")]
+        got = list(e[q]) + list(b[q])
+        for w_, g_ in zip(want, got):
+            assert np.asarray(g_, dtype=dtype).tobytes() == w_.tobytes()
+    e1, b1 = gather_fields(f, ps[0])
+    assert e1.shape == (3,) and b1.shape == (3,)
