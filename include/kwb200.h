@@ -168,6 +168,11 @@ int kwb_fields_ampere(const kwb_grid *g, void *const E[3], void *const B[3],
 int kwb_enable_peer_access(int32_t peer_device);
 int kwb_copy_async(void *dst, const void *src, int64_t bytes, kwb_stream_t stream);
 
+/* Debug builds (make checks: -DKWB_CHECKS): number of failed bounds checks
+ * in the kernels since the last reset (synchronises the device); -1 in a
+ * normal build. */
+int64_t kwb_check_failures(int32_t reset);
+
 /* Start of a step: J = 0 (J may be NULL to skip) and n_status status words
  * = 0, in one kernel (pic/sim.py:138-140). */
 int kwb_zero_step(const kwb_grid *g, void *const J[3], int32_t *status, int32_t n_status,

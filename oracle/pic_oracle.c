@@ -130,7 +130,7 @@ void orc_unlink_empty(orc_pool *pl, int64_t n_sc) {
 
 /* ---- test support: the GPU's shared-reciprocal division ------------------
  * The CUDA advance computes the push's and the move's three quotients by one
- * divisor as q0 = RN(a r), e = fma(-q0, b, a), q = e == 0 ? q0 : fma(e, r, q0)
+ * divisor as q0 = RN(a r), e = fma(-q0, b, a), q = copysign(fma(e, r, q0), a)
  * with r = RN(1 / b) (Markstein).  This checks that construction against
  * IEEE a / b on n pseudo-random pairs drawn like the kernel's operands:
  * numerators of either sign over 2^-40 .. 2^4 (including exact zeros of
@@ -151,7 +151,8 @@ int64_t orc_div_rcp_check(int64_t n, uint64_t seed) {
         const double r = 1.0 / b;
         const double q0 = a * r;
         const double e = fma(-q0, b, a);
-        const double q = e == 0.0 ? q0 : fma(e, r, q0);
+        /* b > 0: the quotient carries a's sign (csrc/common.cuh div_rcp) */
+        const double q = copysign(fma(e, r, q0), a);
         const double ref = a / b;
         uint64_t x, y;
         memcpy(&x, &q, 8);
@@ -175,7 +176,8 @@ int64_t orc_div6_check(int64_t n, uint64_t seed) {
         if (((u3 >> 17) & 1023) == 0) a = 0.0;
         const double q0 = a * r;
         const double e = fma(-q0, b, a);
-        const double q = e == 0.0 ? q0 : fma(e, r, q0);
+        /* b > 0: the quotient carries a's sign (csrc/common.cuh div_rcp) */
+        const double q = copysign(fma(e, r, q0), a);
         const double ref = a / b;
         uint64_t x, y;
         memcpy(&x, &q, 8);

@@ -75,6 +75,7 @@ _SIGS = {
     "kwb_zero_step": ([P, P, P, ctypes.c_int32, P], ctypes.c_int),
     "kwb_enable_peer_access": ([ctypes.c_int32], ctypes.c_int),
     "kwb_copy_async": ([P, P, I64, P], ctypes.c_int),
+    "kwb_check_failures": ([ctypes.c_int32], ctypes.c_int64),
     "kwb_charge_density": ([P, P, P, ctypes.c_int, P, P], ctypes.c_int),
     "kwb_continuity_residual": ([P, P, P, Ptr3, Ptr3, P, P, P], ctypes.c_int),
     "kwb_particle_moments": ([P, P, P, P, P], ctypes.c_int),

@@ -227,6 +227,48 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
 // shared by every component with the same stagger on that axis (CSE).
 // All eight corner loads are issued before the arithmetic (measured: the
 // compiler then overlaps them with the other components' math).
+// Floor-free form of the same sample, bit for bit: the particle sits in
+// cell c with px = RN(c + o), o in [0, 1], so t = px - s (s = 1/2 or 1) lies
+// in [c - 1, c + 1) and floor(t) = (t >= c ? c : c - 1) -- one compare and a
+// select of the precomputed doubles c, c - 1 replace F2I/I2F, and the tile
+// index is the lane's base plus the 0/1 carries.  f = t - floor(t) is the
+// reference's exact difference.  Computed once per (axis, stagger) pair and
+// shared by the components.
+struct AxFrac {
+    double f;
+    int h;
+};
+__device__ __forceinline__ AxFrac ax_frac(double p, double s, double c, double cm1) {
+    const double t = p - s;
+    const bool h = t >= c;
+    return AxFrac{t - (h ? c : cm1), h ? 1 : 0};
+}
+template <int C, typename TT>
+__device__ __forceinline__ double sample_sel(const TT *__restrict__ T, const AxFrac (&ax)[3][2],
+                                             int base, int tx, int txy, int TV) {
+    const AxFrac &X = ax[0][stagger(C, 0) == 1.0], &Y = ax[1][stagger(C, 1) == 1.0],
+                 &Z = ax[2][stagger(C, 2) == 1.0];
+    const double fx = X.f, fy = Y.f, fz = Z.f;
+    const int i00 = base + Z.h * txy + Y.h * tx + X.h;
+#ifdef KWB_CHECKS
+    // the tile holds (sc + 2)^3 points per component; the far corner is
+    // i00 + txy + tx + 1 (T points at component C's tile)
+    if (!KWB_IN(i00 >= 0 && i00 + txy + tx + 1 < TV)) return 0.0;
+#else
+    (void)TV;
+#endif
+    const TT *r00 = T + i00, *r10 = r00 + tx, *r01 = r00 + txy,
+             *r11 = r01 + tx;
+    const double a00 = r00[0], b00 = r00[1], a10 = r10[0], b10 = r10[1];   // (x, x+1) corners
+    const double a01 = r01[0], b01 = r01[1], a11 = r11[0], b11 = r11[1];
+    const double gx = 1.0 - fx;
+    const double c00 = a00 * gx + b00 * fx;
+    const double c10 = a10 * gx + b10 * fx;
+    const double c01 = a01 * gx + b01 * fx;
+    const double c11 = a11 * gx + b11 * fx;
+    return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz;
+}
+
 template <int C, typename TT>
 __device__ __forceinline__ double sample_tile(const TT *__restrict__ T, double px, double py,
                                               double pz, int ox0, int oy0, int oz0, int tx,
@@ -317,7 +359,9 @@ __device__ __noinline__ void deposit_cross_compact(F *__restrict__ jt, int jx, i
 #pragma unroll
                         for (int ja = 0; ja < NS; ++ja) {
                             const CT val = P[0][ja] * T;
-                            if (ja < nac && val != CT(0)) atomicAdd(q + (ja + 1) * sa, (F)val);
+                            F *dst = q + (ja + 1) * sa;
+                            if (ja < nac && val != CT(0) && KWB_IN(dst >= jt && dst < jt + 3 * JV))
+                                atomicAdd(dst, (F)val);
                         }
                     }
                 }
@@ -424,7 +468,7 @@ __device__ __noinline__ void deposit_warp(F *__restrict__ jt, int jx, int jy, in
                     if (c == 0) o = ((j2 + 1) * jy + (j1 + 1)) * jx + (ja + 1);
                     else if (c == 1) o = ((j1 + 1) * jy + (ja + 1)) * jx + (j2 + 1);
                     else o = ((ja + 1) * jy + (j2 + 1)) * jx + (j1 + 1);
-                    atomicAdd(Jc + o, (F)val);
+                    if (KWB_IN(Jc + o >= jt && Jc + o < jt + 3 * JV)) atomicAdd(Jc + o, (F)val);
                 }
             }
         }
@@ -491,7 +535,8 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
 #pragma unroll
             for (int j2 = 0; j2 < 3; ++j2) {
                 const CT T = u * s0q[j2] + v * dsq[j2];
-                atomicAdd(J + (j1 + 1) * s1_ + (j2 + 1) * s2_ + (ja + 1) * sk, (F)(Pout * T));
+                F *dst = J + (j1 + 1) * s1_ + (j2 + 1) * s2_ + (ja + 1) * sk;
+                if (KWB_IN(dst >= jt && dst < jt + 3 * JV)) atomicAdd(dst, (F)(Pout * T));
             }
         }
     }
@@ -516,9 +561,11 @@ __device__ __noinline__ void deposit_cross1(F *__restrict__ jt, int jx, int jy, 
         for (int j2 = 0; j2 < 3; ++j2) {
             const CT T = u * s0o[j2] + v * dso[j2];
             F *p = J + (j1 + 1) * sk + (j2 + 1) * so;
-            atomicAdd(p + sa, (F)(P0 * T));
-            atomicAdd(p + 2 * sa, (F)(P1 * T));
-            atomicAdd(p + 3 * sa, (F)(P2 * T));
+            if (KWB_IN(p + sa >= jt && p + 3 * sa < jt + 3 * JV)) {
+                atomicAdd(p + sa, (F)(P0 * T));
+                atomicAdd(p + 2 * sa, (F)(P1 * T));
+                atomicAdd(p + 3 * sa, (F)(P2 * T));
+            }
         }
     }
 }
@@ -590,9 +637,19 @@ __device__ __forceinline__ void win_store(float4 *ws, const float2 (&q)[3][3], c
     ws[6 * kMaxCells] = make_float4(r[0][2], r[1][2], r[2][2], 0.0f);
 }
 
+// The old position's weights of the three axes (they depend on the
+// particle's input offsets only; KWB_EARLY_S0 computes them at the top of
+// the loop body, off the push/move dependency chain).
 template <int ORDER>
-__device__ __forceinline__ void deposit_window(RegAcc &R, float4 *ws, float oox, float ooy,
-                                               float ooz, float nox, float noy, float noz,
+__device__ __forceinline__ void old_weights(float oox, float ooy, float ooz, float (&s0)[3][3]) {
+    wref3<ORDER, float>((double)oox, 0.0, s0[0]);
+    wref3<ORDER, float>((double)ooy, 0.0, s0[1]);
+    wref3<ORDER, float>((double)ooz, 0.0, s0[2]);
+}
+
+template <int ORDER>
+__device__ __forceinline__ void deposit_window(RegAcc &R, float4 *ws, const float (&s0in)[3][3],
+                                               float nox, float noy, float noz,
                                                float fwx, float fwy, float fwz, int dcx, int dcy,
                                                int dcz) {
 #ifdef KWB_WIN_SMEM
@@ -605,12 +662,13 @@ __device__ __forceinline__ void deposit_window(RegAcc &R, float4 *ws, float oox,
 #endif
     float s0[3][3], ds[3][3], dm2[3], rs[3];
     {
-        const float oo[3] = {oox, ooy, ooz}, no[3] = {nox, noy, noz};
+        const float no[3] = {nox, noy, noz};
         const int dc[3] = {dcx, dcy, dcz};
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             float s1[3];
-            wref3<ORDER, float>((double)oo[a], 0.0, s0[a]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s0[a][k] = s0in[a][k];
             const double c = (double)dc[a];
             wref3<ORDER, float>(c + (double)no[a], c, s1);   // own points dc-1 .. dc+1
             const float w0 = dc[a] == 0 ? s1[0] : (dc[a] > 0 ? 0.0f : s1[1]);
@@ -750,7 +808,11 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
 // One group: all loads, then all stores (entries of a group never alias
 // across the warp's lanes), so the N read-add-writes overlap.
 template <int N>
-__device__ __forceinline__ void box_group(float *b, int stride, const float (&v)[N]) {
+__device__ __forceinline__ void box_group(float *b, int stride, const float (&v)[N],
+                                          const float *box = nullptr) {
+#ifdef KWB_CHECKS
+    if (box && !KWB_IN(b >= box && b + (N - 1) * stride < box + kBoxFloats)) return;
+#endif
     const unsigned a = (unsigned)__cvta_generic_to_shared(b);
     float o[N];
 #pragma unroll
@@ -760,7 +822,9 @@ __device__ __forceinline__ void box_group(float *b, int stride, const float (&v)
     for (int i = 0; i < N; ++i)
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u * i * stride), "f"(__fadd_rn(o[i], v[i]))
                      : "memory");
+#ifndef KWB_EXP_NO_BOX_SYNCWARP   // negative control of the race test (tools/gpurun/r02f.sh)
     __syncwarp();   // measured: without it lanes lose updates (tests/test_gpu_dense.py)
+#endif
 }
 
 // PCS weights (the reference's recipe) at own points -2..2
@@ -826,7 +890,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
                 float v[5];
 #pragma unroll
                 for (int j2 = 0; j2 < 5; ++j2) v[j2] = pa[0] * T[j2];
-                box_group<5>(b + ja, 96, v);
+                box_group<5>(b + ja, 96, v, box);
                 pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3]; pa[3] = pa[4];
             }
             b += 12;
@@ -856,7 +920,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
                 float v[5];
 #pragma unroll
                 for (int j1 = 0; j1 < 5; ++j1) v[j1] = pa[0] * T[j1];
-                box_group<5>(b + 12 * ja, 96, v);
+                box_group<5>(b + 12 * ja, 96, v, box);
                 pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3]; pa[3] = pa[4];
             }
             b += 1;
@@ -886,7 +950,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
                 float v[5];
 #pragma unroll
                 for (int ja = 0; ja < 5; ++ja) v[ja] = P[2][ja] * T;
-                box_group<5>(b + 12 * j2, 96, v);
+                box_group<5>(b + 12 * j2, 96, v, box);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) { y0[j] = y0[j + 1]; y1[j] = y1[j + 1]; }
             }
@@ -1026,6 +1090,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
     const double cxd = (double)cx, cyd = (double)cy, czd = (double)cz;
     const int txy = L.tx * L.ty;
+    const int tbase = (lz * L.ty + ly) * L.tx + lx;   // tile index of (cell - 1) on each axis
     const EB *EBx = ebd, *EBy = ebd + L.TV, *EBz = ebd + 2 * L.TV, *BBx = ebd + 3 * L.TV,
                  *BBy = ebd + 4 * L.TV, *BBz = ebd + 5 * L.TV;
     int fo = 0;      // stayers written to the front of this column
@@ -1115,14 +1180,29 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         if (active) {
             // -- gather (pic/kernels.py:53-77): f64 compute, F store --------
             const double px = cxd + (double)ox, py = cyd + (double)oy, pz = czd + (double)oz;
+#ifdef KWB_EARLY_S0
+            float s0w[3][3];
+            if constexpr (REGACC && sizeof(F) == 4) old_weights<ORDER>((float)ox, (float)oy, (float)oz, s0w);
+#endif
             const int ox0 = orgx - 1, oy0 = orgy - 1, oz0 = orgz - 1;
-#ifndef KWB_EXP_NOGATHER
+#if defined(KWB_GATHER_FLOOR)
             const F e0 = (F)sample_tile<0>(EBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F e1 = (F)sample_tile<1>(EBy, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F e2 = (F)sample_tile<2>(EBz, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F b0 = (F)sample_tile<3>(BBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F b1 = (F)sample_tile<4>(BBy, px, py, pz, ox0, oy0, oz0, L.tx, txy);
             const F b2 = (F)sample_tile<5>(BBz, px, py, pz, ox0, oy0, oz0, L.tx, txy);
+#elif !defined(KWB_EXP_NOGATHER)
+            (void)ox0; (void)oy0; (void)oz0;
+            const AxFrac ax[3][2] = {{ax_frac(px, 0.5, cxd, cxd - 1.0), ax_frac(px, 1.0, cxd, cxd - 1.0)},
+                                     {ax_frac(py, 0.5, cyd, cyd - 1.0), ax_frac(py, 1.0, cyd, cyd - 1.0)},
+                                     {ax_frac(pz, 0.5, czd, czd - 1.0), ax_frac(pz, 1.0, czd, czd - 1.0)}};
+            const F e0 = (F)sample_sel<0>(EBx, ax, tbase, L.tx, txy, L.TV);
+            const F e1 = (F)sample_sel<1>(EBy, ax, tbase, L.tx, txy, L.TV);
+            const F e2 = (F)sample_sel<2>(EBz, ax, tbase, L.tx, txy, L.TV);
+            const F b0 = (F)sample_sel<3>(BBx, ax, tbase, L.tx, txy, L.TV);
+            const F b1 = (F)sample_sel<4>(BBy, ax, tbase, L.tx, txy, L.TV);
+            const F b2 = (F)sample_sel<5>(BBz, ax, tbase, L.tx, txy, L.TV);
 #else   // timing experiment only: no field gather
             const F e0 = (F)(px * 1e-30), e1 = (F)(py * 1e-30), e2 = (F)(pz * 1e-30);
             const F b0 = e0, b1 = e1, b2 = e2;
@@ -1198,11 +1278,16 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 // the owner's register window, for crossers too; what a
                 // crosser deposits outside it goes through the queue
                 const double ww = (double)w;
-                if constexpr (sizeof(F) == 4)
-                    deposit_window<ORDER>(R, wsm, (float)ox, (float)oy, (float)oz, (float)nox,
+                if constexpr (sizeof(F) == 4) {
+#ifndef KWB_EARLY_S0
+                    float s0w[3][3];
+                    old_weights<ORDER>((float)ox, (float)oy, (float)oz, s0w);
+#endif
+                    deposit_window<ORDER>(R, wsm, s0w, (float)nox,
                                         (float)noy, (float)noz, (float)(sp.fac[0] * ww),
                                         (float)(sp.fac[1] * ww), (float)(sp.fac[2] * ww),
                                         dcx, dcy, dcz);
+                }
                 else
                     deposit_window_d<ORDER>(R, (double)ox, (double)oy, (double)oz, (double)nox,
                                           (double)noy, (double)noz, sp.fac[0] * ww,
@@ -1220,7 +1305,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
         // ---- crossing particles -> this warp's queue (no atomics) ---------
         const unsigned qmask = __ballot_sync(0xffffffffu, queue);
-        if (queue) {
+        if (queue && KWB_IN(qidx(wq + __popc(qmask & ((1u << lane) - 1u))) < kQ)) {
             const int j = qidx(wq + __popc(qmask & ((1u << lane) - 1u)));
             q_f[0 * QS + j] = ox; q_f[1 * QS + j] = oy; q_f[2 * QS + j] = oz;
             q_f[3 * QS + j] = nox; q_f[4 * QS + j] = noy; q_f[5 * QS + j] = noz;
@@ -1257,7 +1342,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 const int slot = atomicAdd(&arr[nlc], 1);
                 if (slot < K) { frame = K - 1 - slot; cell = nlc; }
             }
-            if (frame >= 0) {
+            if (frame >= 0 && KWB_IN(frame < K && cell < V)) {
                 const int64_t o = ((int64_t)sc * K + frame) * V + cell;
                 out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
                 out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
@@ -1307,7 +1392,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #pragma unroll
                         for (int c = 0; c < 3; ++c) {
                             F *p = Jb + c * L.JV + regacc_offset(c, a + 1, b + 1, d + 1, L.jx, L.jy);
-                            *p = *p + (F)R.get(c, a, b, d);
+                            if (KWB_IN(p >= jt && p < jt + 3 * L.JV)) *p = *p + (F)R.get(c, a, b, d);
                         }
                     }
                     __syncthreads();
@@ -1326,7 +1411,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             if (v != 0.0f) {
                 const int c = e / 480, r = e - c * 480;
                 const int X = r % 12, Y = (r / 12) % 8, Z = r / 96;
-                atomicAdd(jt + c * L.JV + ((Z + z0 + 1) * L.jy + (Y + y0 + 1)) * L.jx + (X + 1), v);
+                const int o = c * L.JV + ((Z + z0 + 1) * L.jy + (Y + y0 + 1)) * L.jx + (X + 1);
+                if (KWB_IN(o >= 0 && o < 3 * L.JV)) atomicAdd(jt + o, v);
             }
         }
     }

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "kwb200.h"
@@ -13,6 +14,26 @@
 namespace kwb {
 
 constexpr int kThreads = 256;  // one CTA per super cell, 8 warps
+
+// ---- KWB_CHECKS: the bounds-checked debug build --------------------------
+// (compute-sanitizer is not available on the GPU pool.)  Every shared- and
+// global-memory index the kernels compute is checked against its array
+// before the access; a failing check skips the access, counts into a
+// per-module device counter and prints its first occurrence.  Read and reset
+// through kwb_check_failures() (tests/conftest.py asserts 0 after every GPU
+// test when the library was built with the checks).  Compiled out otherwise.
+#ifdef KWB_CHECKS
+static __device__ unsigned long long kwb_chk_count;
+__device__ __forceinline__ bool kwb_chk(bool ok, const char *what, int line) {
+    if (!ok && atomicAdd(&kwb_chk_count, 1ull) == 0ull)
+        printf("KWB_CHECK failed: %s (line %d) block %d thread %d\n", what, line, blockIdx.x,
+               threadIdx.x);
+    return ok;
+}
+#define KWB_IN(cond) kwb::kwb_chk((cond), #cond, __LINE__)
+#else
+#define KWB_IN(cond) true
+#endif
 
 // Python floor-mod (non-negative for n > 0).
 __host__ __device__ __forceinline__ int pymod(int a, int n) {
@@ -30,10 +51,18 @@ __host__ __device__ __forceinline__ int pymod(int a, int n) {
 // CPU suite, oracle orc_div_rcp_check).  An exact q0 is returned as is (the
 // FMA would turn -0 into +0).  The theorem needs no overflow or subnormal
 // intermediates: the operands are O(1) momenta, fields and cell sizes.
+// Every divisor here is positive (gamma, 1 + t^2, cell sizes, 6), so the
+// quotient has the numerator's sign -- zeros included, where the FMA alone
+// would turn -0 / b into +0: the sign is copied from a (one LOP3 instead of
+// a compare and two selects).
 __device__ __forceinline__ double div_rcp(double a, double b, double r) {
     const double q0 = a * r;
     const double e = __fma_rn(-q0, b, a);
+#ifdef KWB_DIV_SELECT
     return e == 0.0 ? q0 : __fma_rn(e, r, q0);   // e == 0: q0 exact, keeps -0 / b = -0
+#else
+    return copysign(__fma_rn(e, r, q0), a);
+#endif
 }
 
 // Field index for the x-fastest layout: (k * ny + j) * nx + i.

@@ -447,3 +447,18 @@ extern "C" int kwb_field_stats(const kwb_grid *g, void *const E[3], void *const 
         field_stats_kernel<double><<<grid_blocks(ncell), 256, 0, s>>>(geo, f3<double>(E), f3<double>(B), out);
     return kwb_check_launch("field_stats_kernel");
 }
+
+unsigned long long kwb_chk_read_fields(int reset) {
+#ifdef KWB_CHECKS
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, kwb::kwb_chk_count, sizeof(v));
+    if (reset) {
+        const unsigned long long z = 0;
+        cudaMemcpyToSymbol(kwb::kwb_chk_count, &z, sizeof(z));
+    }
+    return v;
+#else
+    (void)reset;
+    return 0;
+#endif
+}

@@ -96,3 +96,18 @@ extern "C" int kwb_init_khi(const kwb_grid *g, const kwb_init *ini, const kwb_st
         init_khi_kernel<double><<<blocks, 256, 0, s>>>(geo, *ini, store_of<double>(*st));
     return kwb_check_launch("init_khi_kernel");
 }
+
+unsigned long long kwb_chk_read_init(int reset) {
+#ifdef KWB_CHECKS
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, kwb::kwb_chk_count, sizeof(v));
+    if (reset) {
+        const unsigned long long z = 0;
+        cudaMemcpyToSymbol(kwb::kwb_chk_count, &z, sizeof(z));
+    }
+    return v;
+#else
+    (void)reset;
+    return 0;
+#endif
+}

@@ -46,6 +46,7 @@ __global__ void shift_kernel(StoreT<F> out, ExchT<F> ex, Geo g, int32_t *__restr
         const int bx = d % g.gx, by = (d / g.gx) % g.gy, bz = d / (g.gx * g.gy);
         const int c = (ex.cx[i] - bx * g.scx) +
                       g.scx * ((ex.cy[i] - by * g.scy) + g.scy * (ex.cz[i] - bz * g.scz));
+        if (!KWB_IN(d >= 0 && d < g.gx * g.gy * g.gz && c >= 0 && c < V)) continue;
         const int64_t colx = (int64_t)d * V + c;
         const int slot = atomicAdd(&out.back[colx], 1);
         const int fill = out.front[colx] + slot + 1;
@@ -123,6 +124,7 @@ __global__ void export_kernel(Geo g, StoreT<F> st, int64_t col0, int64_t col1,
                   z = bz * g.scz + c / (g.scx * g.scy);
         const int f = st.front[colx], b = st.back[colx];
         int64_t o = cell_start[colx - col0];
+        if (!KWB_IN(f >= 0 && b >= 0 && f + b <= K)) continue;
         for (int j = 0; j < f + b; ++j, ++o) {
             const int k = j < f ? j : K - b + (j - f);
             const int64_t q = ((int64_t)s * K + k) * V + c;
@@ -171,13 +173,15 @@ __global__ void export_sc_kernel(Geo g, StoreT<F> st, int64_t col0, const int64_
         for (int a = 0; a < 10; ++a) {
             if (a < 3) {
                 const int v = a == 0 ? x : a == 1 ? y : z;
-                for (int j = j0; j < j1; ++j) bi[my0 + j - base] = v;
+                for (int j = j0; j < j1; ++j)
+                    if (KWB_IN(my0 + j - base >= 0 && my0 + j - base < m)) bi[my0 + j - base] = v;
             } else {
                 const F *src = a == 3 ? st.ox : a == 4 ? st.oy : a == 5 ? st.oz : a == 6 ? st.ux
                              : a == 7 ? st.uy : a == 8 ? st.uz : st.w;
                 for (int j = j0; j < j1; ++j) {
                     const int k = j < f ? j : K - b + (j - f);
-                    bf[my0 + j - base] = src[(s * K + k) * V + t];
+                    if (KWB_IN(my0 + j - base >= 0 && my0 + j - base < m && k >= 0 && k < K))
+                        bf[my0 + j - base] = src[(s * K + k) * V + t];
                 }
             }
             __syncthreads();
@@ -206,6 +210,7 @@ __global__ void repack_kernel(Geo g, StoreT<F> src, StoreT<F> dst) {
          colx += (int64_t)gridDim.x * blockDim.x) {
         const int s = (int)(colx / V), c = (int)(colx % V);
         const int f = src.front[colx], b = src.back[colx];
+        if (!KWB_IN(f >= 0 && b >= 0 && f + b <= Ks)) continue;
         const int n = min(f + b, Kd);
         for (int j = 0; j < n; ++j) {
             const int k = j < f ? j : Ks - b + (j - f);
@@ -224,6 +229,7 @@ template <typename F, typename Fn>
 __device__ __forceinline__ void for_column(const StoreT<F> &st, int s, int c, int V, Fn fn) {
     const int64_t colx = (int64_t)s * V + c;
     const int f = st.front[colx], b = st.back[colx], K = st.frames;
+    if (!KWB_IN(f >= 0 && b >= 0 && f + b <= K)) return;
     for (int j = 0; j < f + b; ++j) {
         const int k = j < f ? j : K - b + (j - f);
         fn(((int64_t)s * K + k) * V + c);
@@ -370,6 +376,31 @@ static int check_store(const kwb_store *s, const char *what) {
         return KWB_EINVAL;
     }
     return KWB_OK;
+}
+
+// KWB_CHECKS counters of the three modules (0 in a normal build).
+#ifdef KWB_CHECKS
+static unsigned long long chk_read(int reset) {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, kwb_chk_count, sizeof(v));
+    if (reset) {
+        const unsigned long long z = 0;
+        cudaMemcpyToSymbol(kwb_chk_count, &z, sizeof(z));
+    }
+    return v;
+}
+#endif
+unsigned long long kwb_chk_read_fields(int reset);
+unsigned long long kwb_chk_read_init(int reset);
+
+extern "C" int64_t kwb_check_failures(int32_t reset) {
+#ifdef KWB_CHECKS
+    cudaDeviceSynchronize();
+    return (int64_t)(chk_read(reset) + kwb_chk_read_fields(reset) + kwb_chk_read_init(reset));
+#else
+    (void)reset;
+    return -1;   // not a checks build
+#endif
 }
 
 static int block_threads(const kwb_grid *g) {

@@ -35,3 +35,18 @@ def oracle_lib():
     from oracle import pic
     pic.build()
     return pic
+
+
+@pytest.fixture(autouse=True)
+def _kernel_bounds_checks(request):
+    """With the bounds-checked debug library (make -C paper_1606_02862_b200/csrc
+    checks; KWB_LIB_PATH=exp/libkwb200_checks.so), every GPU test must leave
+    zero failed index checks in the kernels (compute-sanitizer stand-in)."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    from paper_1606_02862_b200 import _lib
+    if _lib._lib is None:
+        return
+    n = int(_lib._lib.kwb_check_failures(1))
+    assert n <= 0, f"{n} kernel bounds check(s) failed (KWB_CHECKS build)"
