@@ -197,9 +197,10 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     L.jx = scx + 2 * H; L.jy = scy + 2 * H; L.jz = scz + 2 * H; L.JV = L.jx * L.jy * L.jz;
     using C = AdvCfg<F, ORDER>;
     size_t o = (size_t)6 * L.TV * sizeof(typename C::EB);
+    o = (o + 127) & ~size_t(127);   // TMA source/destination: 128-byte aligned
     L.off_jt = o;
     o += (size_t)3 * L.JV * sizeof(F);
-    o = (o + 15) & ~size_t(15);
+    o = (o + 127) & ~size_t(127);
     L.off_qf = o;
     o += (size_t)7 * kWarps * C::kQ * sizeof(F);
     L.off_qi = o;
@@ -961,14 +962,62 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
     }
 }
 
+// ---- TMA (tensor memory accelerator) helpers -----------------------------
+constexpr int TMA_EB = 1, TMA_J = 2;
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *m, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                            int c3, uint64_t *m) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(m))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_4d(const CUtensorMap *tm, int c0, int c1, int c2,
+                                                  int c3, const void *src) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group"
+        " [%0, {%1, %2, %3, %4}], [%5];" ::"l"(reinterpret_cast<uint64_t>(tm)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
 __global__ void __launch_bounds__(kMaxCells, AdvCfg<F, ORDER>::kMinBlocks)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
-               int32_t *__restrict__ status) {
+               int32_t *__restrict__ status, const __grid_constant__ CUtensorMap tm_eb,
+               const __grid_constant__ CUtensorMap tm_j, int tma) {
     constexpr int H = Shape<ORDER>::H;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ int s_maxcol;
+    __shared__ __align__(8) uint64_t s_mbar;   // TMA completion of the E/B tile
 
     const int scx = SX ? SX : g.scx, scy = SY ? SY : g.scy, scz = SZ ? SZ : g.scz;
     const int V = scx * scy * scz;
@@ -1027,6 +1076,27 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     };
     prefetch(0);   // issued before the staging: its latency overlaps it
 
+    // TMA for super cells whose E/B guard and J halo lie inside the grid (no
+    // periodic wrap; the seams keep the indexed path): one elected thread
+    // loads the 6-lattice E/B box (cp.async.bulk.tensor, completion on an
+    // mbarrier) and, at the end, reduce-adds the J tile into the lattices
+    // (cp.reduce.async.bulk.tensor) -- kwb_particles_advance builds the two
+    // tensor maps when the lattices are equally spaced (TMA_EB / TMA_J).
+    const bool interior = bx >= 1 && bx + 2 <= g.gx && by >= 1 && by + 2 <= g.gy && bz >= 1 &&
+                          bz + 2 <= g.gz;
+    const bool tma_eb = REGACC && (tma & TMA_EB) && interior;
+    const bool tma_j = sizeof(F) == 4 && REGACC && (tma & TMA_J) && interior && !fp.jpl;
+    // f32: the box lands in the (still unused) queue area and is widened into
+    // the float64 tile; f64: straight into the tile (same layout)
+    void *eb_dst = sizeof(F) == 4 ? (void *)(smem_raw + L.off_qf) : (void *)ebd;
+    if (tma_eb && t == 0) {
+        mbar_init(&s_mbar, 1);
+        fence_mbar_init();
+        const int boxx = sizeof(F) == 4 ? (L.tx * 4 + 15) / 16 * 4 : L.tx;
+        mbar_expect_tx(&s_mbar, (unsigned)(6 * boxx * L.ty * L.tz * sizeof(F)));
+        tma_load_4d(eb_dst, &tm_eb, orgx - 1, orgy - 1, orgz - 1, 0, &s_mbar);
+    }
+
     // ---- periodic index tables, then stage E/B and clear the J tile -------
     for (int i = t; i < L.tx; i += blockDim.x) wtx[i] = pymod(orgx - 1 + i, g.nx);
     for (int i = t; i < L.ty; i += blockDim.x) wty[i] = pymod(orgy - 1 + i, g.ny);
@@ -1042,7 +1112,20 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     if constexpr (PCSBOX)
         for (int i = lane; i < kBoxFloats; i += 32) wbox[i] = 0.0f;
     __syncthreads();
-    {
+    if (tma_eb) {
+        mbar_wait(&s_mbar, 0);
+        if constexpr (sizeof(F) == 4) {   // widen the float box (x padded to 16 B) into the tile
+            const int boxx = (L.tx * 4 + 15) / 16 * 4;
+            const float *src = reinterpret_cast<const float *>(eb_dst);
+            const int total = 6 * L.TV, txy_ = L.tx * L.ty;
+            for (int i = t; i < total; i += blockDim.x) {
+                const int c = i / L.TV, r = i - c * L.TV;
+                const int d = r / txy_, r2 = r - d * txy_;
+                const int b = r2 / L.tx, a = r2 - b * L.tx;
+                ebd[i] = (EB)src[((c * L.tz + d) * L.ty + b) * boxx + a];
+            }
+        }
+    } else {
         // flat over (component, z, y, x) so every lane works, and batches of
         // kStageB independent loads in flight per thread (one memory latency
         // per batch instead of one per tile row)
@@ -1416,16 +1499,21 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             }
         }
     }
+    if (tma_j) fence_proxy_async();   // this thread's J tile writes -> the async proxy
     __syncthreads();
 
-    // ---- flush the J tile: coalesced red.global.add of non-zero entries ---
+    // ---- flush the J tile: one TMA reduce-add (interior), else coalesced
+    // red.global.add of the non-zero entries ---------------------------------
     auto jrow = [&](int c, int d, int b) -> F * {   // row (tile z d, tile y b) of J[c]
         if (fp.jpl)
             return (F *)fp.jpl[c * g.nz + wjz[d]] + (int64_t)wjy[b] * g.nx;
         F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
         return dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
     };
-    if (sizeof(F) == 4 && (L.jx & 1) == 0) {
+    if (tma_j) {
+        // the tile's smem must stay valid until the bulk read completes
+        if (t == 0) tma_reduce_add_4d(&tm_j, orgx - H, orgy - H, orgz - H, 0, jt);
+    } else if (sizeof(F) == 4 && (L.jx & 1) == 0) {
         // x-adjacent pairs with one red.global.add.v2.f32 where the pair is
         // contiguous and 8-byte aligned in J (not across the periodic seam)
         const int total = 3 * L.JV / 2, nth = blockDim.x, jxy = L.jx * L.jy;

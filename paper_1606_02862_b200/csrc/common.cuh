@@ -5,6 +5,7 @@
 // particle state is to stay bitwise equal.
 #pragma once
 
+#include <cuda.h>   // CUtensorMap (types only; the encoder comes from cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <stdint.h>

@@ -25,6 +25,8 @@
 //  * The J tile (super cell + shape halo) is flushed once with coalesced
 //    red.global.add; leavers of the super cell go to an exchange buffer.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -408,6 +410,52 @@ static int block_threads(const kwb_grid *g) {
     return (V + 31) / 32 * 32;
 }
 
+// ---- TMA tensor maps of the field lattices ---------------------------------
+// The encoder is a driver entry point (no -lcuda): cudaGetDriverEntryPoint.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// n lattices at base, base + L, ..., L = one lattice's bytes, each (nx, ny,
+// nz) x fastest: a 4-D map (x, y, z, lattice) with the given box.  false when
+// the layout does not qualify (not equally spaced / not 16-byte multiples).
+template <typename F>
+static bool lattice_map(CUtensorMap *m, void *const *ptrs, int n, const kwb_grid *g,
+                        const cuuint32_t box[4]) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || getenv("KWB_NO_TMA")) return false;
+    const cuuint64_t L = (cuuint64_t)g->nx * g->ny * g->nz * sizeof(F);
+    const uintptr_t base = (uintptr_t)ptrs[0];
+    for (int i = 0; i < n; ++i)
+        if ((uintptr_t)ptrs[i] != base + i * L) return false;
+    if (base % 16 || ((cuuint64_t)g->nx * sizeof(F)) % 16 || L % 16 || (box[0] * sizeof(F)) % 16)
+        return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)g->nx, (cuuint64_t)g->ny, (cuuint64_t)g->nz,
+                                (cuuint64_t)n};
+    const cuuint64_t strides[3] = {(cuuint64_t)g->nx * sizeof(F),
+                                   (cuuint64_t)g->nx * g->ny * sizeof(F), L};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, sizeof(F) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+              4, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
 static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex, void *const E[3],
@@ -429,8 +477,28 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
     if (cudaMemsetAsync(ex->count, 0, sizeof(int32_t), stream) != cudaSuccess)
         return kwb_check_launch("exchange counter reset");
     const int n_sc = g->gx * g->gy * g->gz;
+    // E/B box: the tile (super cell + 1 guard), x padded to 16 bytes; J box:
+    // the J tile (super cell + shape halo) -- float32 J only (TMA reduce-add)
+    CUtensorMap tm_eb, tm_j;
+    memset(&tm_eb, 0, sizeof(tm_eb));
+    memset(&tm_j, 0, sizeof(tm_j));
+    int tma = 0;
+    if (REGACC) {
+        constexpr int H = Shape<ORDER>::H;
+        const cuuint32_t tx = (cuuint32_t)g->scx + 2;
+        const cuuint32_t ebox[4] = {(cuuint32_t)((tx * sizeof(F) + 15) / 16 * 16 / sizeof(F)),
+                                    (cuuint32_t)g->scy + 2, (cuuint32_t)g->scz + 2, 6};
+        void *eb[6] = {E[0], E[1], E[2], B[0], B[1], B[2]};
+        if (ebox[0] <= 256 && ebox[1] <= 256 && lattice_map<F>(&tm_eb, eb, 6, g, ebox))
+            tma |= TMA_EB;
+        const cuuint32_t jbox[4] = {(cuuint32_t)(g->scx + 2 * H), (cuuint32_t)(g->scy + 2 * H),
+                                    (cuuint32_t)(g->scz + 2 * H), 3};
+        if (sizeof(F) == 4 && !jpl && jbox[0] <= 256 && jbox[1] <= 256 &&
+            lattice_map<F>(&tm_j, J, 3, g, jbox))
+            tma |= TMA_J;
+    }
     kern<<<n_sc, threads, smem, stream>>>(geo, *sp, store_of<F>(*in), store_of<F>(*out),
-                                          exch_of<F>(*ex), fp, status);
+                                          exch_of<F>(*ex), fp, status, tm_eb, tm_j, tma);
     return kwb_check_launch("advance_kernel");
 }
 

@@ -20,12 +20,16 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--steps", type=int, default=40)
-    ap.add_argument("libs", nargs="+")
+    ap.add_argument("libs", nargs="+", help="library paths; LIB@VAR=VAL sets an env var for that arm")
     a = ap.parse_args()
     res = {lib: [] for lib in a.libs}
     for r in range(a.rounds):
         for lib in a.libs:
-            env = dict(os.environ, KWB_LIB_PATH=os.path.abspath(lib))
+            path, _, kv = lib.partition("@")
+            env = dict(os.environ, KWB_LIB_PATH=os.path.abspath(path))
+            if kv:
+                k, _, v = kv.partition("=")
+                env[k] = v
             out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", a.config,
                                   "--steps", str(a.steps), "--warmup", "3", "--no-cpu"],
                                  capture_output=True, text=True, env=env, cwd=ROOT)
