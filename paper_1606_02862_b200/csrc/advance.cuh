@@ -189,7 +189,7 @@ struct AdvLayout {
     size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, off_wb, off_ws, bytes;
 };
 
-template <typename F, int ORDER>
+template <typename F, int ORDER, int NS = 1>
 __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     constexpr int H = Shape<ORDER>::H;
     AdvLayout L;
@@ -206,7 +206,7 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     L.off_qi = o;
     o += (size_t)kWarps * C::kQ * sizeof(int);
     L.off_arr = o;
-    o += (size_t)kMaxCells * sizeof(int);
+    o += (size_t)NS * kMaxCells * sizeof(int);   // in-super-cell arrivals per species
     L.off_pf = o;
     o += (size_t)2 * 7 * kMaxCells * sizeof(F);   // double-buffered next-particle records
     L.off_wrap = o;
@@ -963,7 +963,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
 }
 
 // ---- TMA (tensor memory accelerator) helpers -----------------------------
-constexpr int TMA_EB = 1, TMA_J = 2;
+constexpr int TMA_EB = 1;
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -994,35 +994,62 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *tm, in
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(m))
         : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_reduce_add_4d(const CUtensorMap *tm, int c0, int c1, int c2,
-                                                  int c3, const void *src) {
-    asm volatile(
-        "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group"
-        " [%0, {%1, %2, %3, %4}], [%5];" ::"l"(reinterpret_cast<uint64_t>(tm)),
-        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
-        : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+// Lane-level species fusion (NS = 2): one launch advances both species of
+// the super cell -- E/B staged once, one register window and J tile for
+// both, one flush -- and each thread walks its cell's electron column and
+// then its ion column in ONE loop, so a warp's trip count is the longest sum
+// of the two columns instead of the sum of the two longest (Poisson
+// columns: ~9 % fewer rounds).  The species of a lane's current particle
+// selects its pointers and constants from a shared-memory table (a runtime
+// index into the kernel parameters would copy them to local memory).
+template <typename F>
+struct SpeciesB {   // the second species of a fused launch
+    StoreT<F> in, out;
+    kwb_species sp;
+    int32_t *status;
+};
+template <typename F>
+struct SpTab {
+    const F *in[7];
+    F *out[7];
+    int32_t *status;
+    double qm, fac[3];
+    int K;
+};
+template <typename F>
+__device__ __forceinline__ void fill_tab(SpTab<F> &T, const StoreT<F> &in, const StoreT<F> &out,
+                                         const kwb_species &sp, int32_t *status) {
+    T.in[0] = in.ox; T.in[1] = in.oy; T.in[2] = in.oz; T.in[3] = in.ux; T.in[4] = in.uy;
+    T.in[5] = in.uz; T.in[6] = in.w;
+    T.out[0] = out.ox; T.out[1] = out.oy; T.out[2] = out.oz; T.out[3] = out.ux;
+    T.out[4] = out.uy; T.out[5] = out.uz; T.out[6] = out.w;
+    T.status = status;
+    T.qm = sp.qm_half_dt;
+    T.fac[0] = sp.fac[0]; T.fac[1] = sp.fac[1]; T.fac[2] = sp.fac[2];
+    T.K = in.frames;
 }
 
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
-template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
+template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS>
 __global__ void __launch_bounds__(kMaxCells, AdvCfg<F, ORDER>::kMinBlocks)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
-               int32_t *__restrict__ status, const __grid_constant__ CUtensorMap tm_eb,
-               const __grid_constant__ CUtensorMap tm_j, int tma) {
+               int32_t *__restrict__ status, const __grid_constant__ CUtensorMap tm_eb, int tma,
+               SpeciesB<F> sb) {
+    static_assert(NS == 1 || NS == 2, "one or two species per launch");
     constexpr int H = Shape<ORDER>::H;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ int s_maxcol;
+    __shared__ int s_maxcol, s_maxcol1;
     __shared__ __align__(8) uint64_t s_mbar;   // TMA completion of the E/B tile
 
     const int scx = SX ? SX : g.scx, scy = SY ? SY : g.scy, scz = SZ ? SZ : g.scz;
     const int V = scx * scy * scz;
-    const AdvLayout L = adv_layout<F, ORDER>(scx, scy, scz);
+    const AdvLayout L = adv_layout<F, ORDER, NS>(scx, scy, scz);
     const int K = in.frames;
+    __shared__ SpTab<F> tab[NS];
+    if (NS == 2) {
+        if (threadIdx.x == 0) fill_tab(tab[0], in, out, sp, status);
+        if (threadIdx.x == 32) fill_tab(tab[NS - 1], sb.in, sb.out, sb.sp, sb.status);
+    }
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const bool owner = t < V;
     const int sc = blockIdx.x;
@@ -1045,16 +1072,28 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     const int64_t col = (int64_t)sc * V + t;
     const int front_in = owner ? in.front[col] : 0;
     const int back_in = owner ? in.back[col] : 0;
-    const int n_t = front_in + back_in;
+    const int n0 = front_in + back_in;           // this cell's species-0 particles
+    const int front1 = (NS == 2 && owner) ? sb.in.front[col] : 0;
+    const int back1 = (NS == 2 && owner) ? sb.in.back[col] : 0;
+    const int n_t = n0 + front1 + back1;         // the lane's sequence: species 0, then 1
     // empty super cell (e.g. a z-slab guard layer): nothing to stage or deposit
     if (__syncthreads_or(n_t) == 0) {
-        if (owner) { out.front[col] = 0; out.back[col] = 0; }
+        if (owner) {
+            out.front[col] = 0; out.back[col] = 0;
+            if (NS == 2) { sb.out.front[col] = 0; sb.out.back[col] = 0; }
+        }
         return;
     }
+    const int K1 = NS == 2 ? sb.in.frames : K;
 
+    // particle i of the lane's sequence: species (i >= n0), frame slot
+    auto species_of = [&](int i) -> int { return NS == 2 && i >= n0 ? 1 : 0; };
     auto slot_of = [&](int i) -> int64_t {
-        const int k = i < front_in ? i : K - back_in + (i - front_in);
-        return ((int64_t)sc * K + k) * V + t;
+        const int s = species_of(i);
+        const int j = s ? i - n0 : i, fr = s ? front1 : front_in, bk = s ? back1 : back_in;
+        const int Ks = s ? K1 : K;
+        const int k = j < fr ? j : Ks - bk + (j - fr);
+        return ((int64_t)sc * Ks + k) * V + t;
     };
     // next-particle records are copied global -> shared asynchronously
     // (double buffered, this thread's slots only) and read at their uses,
@@ -1064,37 +1103,45 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         if (i < n_t) {
             const int64_t q = slot_of(i);
             F *d = pf + (i & 1) * 7 * kMaxCells;
-            cp_async_elem(d + 0 * kMaxCells, in.ox + q);
-            cp_async_elem(d + 1 * kMaxCells, in.oy + q);
-            cp_async_elem(d + 2 * kMaxCells, in.oz + q);
-            cp_async_elem(d + 3 * kMaxCells, in.ux + q);
-            cp_async_elem(d + 4 * kMaxCells, in.uy + q);
-            cp_async_elem(d + 5 * kMaxCells, in.uz + q);
-            cp_async_elem(d + 6 * kMaxCells, in.w + q);
+            if (NS == 2) {
+                const SpTab<F> &T = tab[species_of(i)];
+#pragma unroll
+                for (int a = 0; a < 7; ++a) cp_async_elem(d + a * kMaxCells, T.in[a] + q);
+            } else {
+                cp_async_elem(d + 0 * kMaxCells, in.ox + q);
+                cp_async_elem(d + 1 * kMaxCells, in.oy + q);
+                cp_async_elem(d + 2 * kMaxCells, in.oz + q);
+                cp_async_elem(d + 3 * kMaxCells, in.ux + q);
+                cp_async_elem(d + 4 * kMaxCells, in.uy + q);
+                cp_async_elem(d + 5 * kMaxCells, in.uz + q);
+                cp_async_elem(d + 6 * kMaxCells, in.w + q);
+            }
         }
         cp_async_commit();
     };
     prefetch(0);   // issued before the staging: its latency overlaps it
 
-    // TMA for super cells whose E/B guard and J halo lie inside the grid (no
-    // periodic wrap; the seams keep the indexed path): one elected thread
-    // loads the 6-lattice E/B box (cp.async.bulk.tensor, completion on an
-    // mbarrier) and, at the end, reduce-adds the J tile into the lattices
-    // (cp.reduce.async.bulk.tensor) -- kwb_particles_advance builds the two
-    // tensor maps when the lattices are equally spaced (TMA_EB / TMA_J).
+    // TMA for super cells whose E/B guard lies inside the grid (no periodic
+    // wrap; the seams keep the indexed path): one elected thread loads the
+    // 6-lattice E/B box (cp.async.bulk.tensor, completion on an mbarrier)
+    // into the still unused queue area, and the CTA widens it into the
+    // float64 tile.  kwb_particles_advance builds the tensor map when the
+    // lattices are equally spaced (TMA_EB).  The box's x start must be
+    // 16-byte aligned on B200 (measured: an unaligned start raises an
+    // illegal-instruction fault, tools/probe/tma_probe2.cu), so it starts
+    // at origin - 4 (f32) / origin - 2 (f64) instead of origin - 1.
     const bool interior = bx >= 1 && bx + 2 <= g.gx && by >= 1 && by + 2 <= g.gy && bz >= 1 &&
                           bz + 2 <= g.gz;
     const bool tma_eb = REGACC && (tma & TMA_EB) && interior;
-    const bool tma_j = sizeof(F) == 4 && REGACC && (tma & TMA_J) && interior && !fp.jpl;
-    // f32: the box lands in the (still unused) queue area and is widened into
-    // the float64 tile; f64: straight into the tile (same layout)
-    void *eb_dst = sizeof(F) == 4 ? (void *)(smem_raw + L.off_qf) : (void *)ebd;
+    constexpr int kTmaX0 = sizeof(F) == 4 ? 4 : 2;        // box x start = origin - kTmaX0
+    const int boxx = (L.tx + kTmaX0 - 1 + (16 / (int)sizeof(F)) - 1) / (16 / (int)sizeof(F)) *
+                     (16 / (int)sizeof(F));                // covers origin - 1 .. origin + scx
+    void *eb_dst = (void *)(smem_raw + L.off_qf);
     if (tma_eb && t == 0) {
         mbar_init(&s_mbar, 1);
         fence_mbar_init();
-        const int boxx = sizeof(F) == 4 ? (L.tx * 4 + 15) / 16 * 4 : L.tx;
         mbar_expect_tx(&s_mbar, (unsigned)(6 * boxx * L.ty * L.tz * sizeof(F)));
-        tma_load_4d(eb_dst, &tm_eb, orgx - 1, orgy - 1, orgz - 1, 0, &s_mbar);
+        tma_load_4d(eb_dst, &tm_eb, orgx - kTmaX0, orgy - 1, orgz - 1, 0, &s_mbar);
     }
 
     // ---- periodic index tables, then stage E/B and clear the J tile -------
@@ -1104,8 +1151,10 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     for (int i = t; i < L.jx; i += blockDim.x) wjx[i] = pymod(orgx - H + i, g.nx);
     for (int i = t; i < L.jy; i += blockDim.x) wjy[i] = pymod(orgy - H + i, g.ny);
     for (int i = t; i < L.jz; i += blockDim.x) wjz[i] = pymod(orgz - H + i, g.nz);
-    if (t < kMaxCells) arr[t] = 0;
-    if (t == 0) s_maxcol = 0;
+    if (t < kMaxCells)
+#pragma unroll
+        for (int s_ = 0; s_ < NS; ++s_) arr[s_ * kMaxCells + t] = 0;
+    if (t == 0) { s_maxcol = 0; s_maxcol1 = 0; }
     for (int i = t; i < 3 * L.JV; i += blockDim.x) jt[i] = F(0);
     constexpr bool PCSBOX = ORDER == 3 && !REGACC && sizeof(F) == 4 && SX == 8 && SY == 8 && SZ == 4;
     float *wbox = reinterpret_cast<float *>(smem_raw + L.off_wb) + wid * kBoxFloats;
@@ -1114,16 +1163,14 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     __syncthreads();
     if (tma_eb) {
         mbar_wait(&s_mbar, 0);
-        if constexpr (sizeof(F) == 4) {   // widen the float box (x padded to 16 B) into the tile
-            const int boxx = (L.tx * 4 + 15) / 16 * 4;
-            const float *src = reinterpret_cast<const float *>(eb_dst);
-            const int total = 6 * L.TV, txy_ = L.tx * L.ty;
-            for (int i = t; i < total; i += blockDim.x) {
-                const int c = i / L.TV, r = i - c * L.TV;
-                const int d = r / txy_, r2 = r - d * txy_;
-                const int b = r2 / L.tx, a = r2 - b * L.tx;
-                ebd[i] = (EB)src[((c * L.tz + d) * L.ty + b) * boxx + a];
-            }
+        // widen / copy the box (x from origin - kTmaX0) into the tile (x from origin - 1)
+        const F *src = reinterpret_cast<const F *>(eb_dst);
+        const int total = 6 * L.TV, txy_ = L.tx * L.ty;
+        for (int i = t; i < total; i += blockDim.x) {
+            const int c = i / L.TV, r = i - c * L.TV;
+            const int d = r / txy_, r2 = r - d * txy_;
+            const int b = r2 / L.tx, a = r2 - b * L.tx;
+            ebd[i] = (EB)src[((c * L.tz + d) * L.ty + b) * boxx + a + kTmaX0 - 1];
         }
     } else {
         // flat over (component, z, y, x) so every lane works, and batches of
@@ -1169,14 +1216,15 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #pragma unroll
         for (int k = 0; k < 7; ++k) wsm[k * kMaxCells] = make_float4(0.f, 0.f, 0.f, 0.f);
 #endif
-    const double qm = sp.qm_half_dt;
+    const double qm0 = sp.qm_half_dt;
     const int cx = orgx + lx, cy = orgy + ly, cz = orgz + lz;
     const double cxd = (double)cx, cyd = (double)cy, czd = (double)cz;
     const int txy = L.tx * L.ty;
     const int tbase = (lz * L.ty + ly) * L.tx + lx;   // tile index of (cell - 1) on each axis
     const EB *EBx = ebd, *EBy = ebd + L.TV, *EBz = ebd + 2 * L.TV, *BBx = ebd + 3 * L.TV,
                  *BBy = ebd + 4 * L.TV, *BBz = ebd + 5 * L.TV;
-    int fo = 0;      // stayers written to the front of this column
+    int fo = 0;      // stayers written to the front of this column (species 0)
+    int fo1 = 0;     // ... species 1 (NS = 2)
     int n_err = 0;
     int wq = 0;      // this warp's queue fill (warp-uniform)
     // PCS: the queue is a ring of kQ (a power of two) records from qh, and
@@ -1188,6 +1236,10 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
     // Deposit the queued crossing particles of this warp (lanes take one
     // record each; CAS into the J tile).
+    // the record's species (bit 30 of its info word) selects the deposit factors
+    auto fac_of = [&](int info, int k) -> double {
+        return NS == 2 ? tab[(info >> 30) & 1].fac[k] : sp.fac[k];
+    };
     auto drain_queue = [&]() {
         __syncwarp();
         auto warp_record = [&](int j) {   // warp-uniform j
@@ -1197,7 +1249,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                                    ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
                                    q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j],
                                    q_f[3 * QS + j], q_f[4 * QS + j], q_f[5 * QS + j],
-                                   q_f[6 * QS + j], sp.fac[0], sp.fac[1], sp.fac[2], true);
+                                   q_f[6 * QS + j], fac_of(info, 0), fac_of(info, 1),
+                                   fac_of(info, 2), true);
         };
         if (!REGACC) {
             // PCS: every particle is queued; one record per lane, loop-rolled
@@ -1209,8 +1262,8 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                     jt, L.jx, L.jy, L.JV, info & 255, (info >> 8) & 255, (info >> 16) & 255,
                     ((info >> 24) & 3) - 1, ((info >> 26) & 3) - 1, ((info >> 28) & 3) - 1,
                     q_f[0 * QS + j], q_f[1 * QS + j], q_f[2 * QS + j], q_f[3 * QS + j],
-                    q_f[4 * QS + j], q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0], sp.fac[1],
-                    sp.fac[2]);
+                    q_f[4 * QS + j], q_f[5 * QS + j], q_f[6 * QS + j], fac_of(info, 0),
+                    fac_of(info, 1), fac_of(info, 2));
             }
         } else {
             // single-axis crossers (the common case): one record per lane,
@@ -1230,8 +1283,9 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                                                  ddx + ddy + ddz, q_f[0 * QS + j],
                                                  q_f[1 * QS + j], q_f[2 * QS + j],
                                                  q_f[3 * QS + j], q_f[4 * QS + j],
-                                                 q_f[5 * QS + j], q_f[6 * QS + j], sp.fac[0],
-                                                 sp.fac[1], sp.fac[2]);
+                                                 q_f[5 * QS + j], q_f[6 * QS + j],
+                                                 fac_of(info, 0), fac_of(info, 1),
+                                                 fac_of(info, 2));
                     } else {
                         multi = true;
                     }
@@ -1249,6 +1303,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
     for (int i = 0; i < n_w; ++i) {
         const bool active = i < n_t;
+        const int sp_i = species_of(i);   // this particle's species (0 unless NS = 2)
         cp_async_wait_all();
         const F *cur = pf + (i & 1) * 7 * kMaxCells;
         prefetch(i + 1);
@@ -1292,6 +1347,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 #endif
 
             // -- Boris push (pic/kernels.py:80-104), all in double ---------
+            const double qm = NS == 2 ? tab[sp_i].qm : qm0;
             const double qe0 = qm * (double)e0, qe1 = qm * (double)e1, qe2 = qm * (double)e2;
             const double umx = (double)ux + qe0;
             const double umy = (double)uy + qe1;
@@ -1361,20 +1417,23 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                 // the owner's register window, for crossers too; what a
                 // crosser deposits outside it goes through the queue
                 const double ww = (double)w;
+                const double f0 = NS == 2 ? tab[sp_i].fac[0] : sp.fac[0];
+                const double f1 = NS == 2 ? tab[sp_i].fac[1] : sp.fac[1];
+                const double f2 = NS == 2 ? tab[sp_i].fac[2] : sp.fac[2];
                 if constexpr (sizeof(F) == 4) {
 #ifndef KWB_EARLY_S0
                     float s0w[3][3];
                     old_weights<ORDER>((float)ox, (float)oy, (float)oz, s0w);
 #endif
                     deposit_window<ORDER>(R, wsm, s0w, (float)nox,
-                                        (float)noy, (float)noz, (float)(sp.fac[0] * ww),
-                                        (float)(sp.fac[1] * ww), (float)(sp.fac[2] * ww),
+                                        (float)noy, (float)noz, (float)(f0 * ww),
+                                        (float)(f1 * ww), (float)(f2 * ww),
                                         dcx, dcy, dcz);
                 }
                 else
                     deposit_window_d<ORDER>(R, (double)ox, (double)oy, (double)oz, (double)nox,
-                                          (double)noy, (double)noz, sp.fac[0] * ww,
-                                          sp.fac[1] * ww, sp.fac[2] * ww, dcx, dcy, dcz);
+                                          (double)noy, (double)noz, f0 * ww,
+                                          f1 * ww, f2 * ww, dcx, dcy, dcz);
 #ifndef KWB_EXP_NOCROSS   // timing experiment only: skip crossing deposits
                 queue = (dcx | dcy | dcz) != 0;
 #endif
@@ -1394,7 +1453,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             q_f[3 * QS + j] = nox; q_f[4 * QS + j] = noy; q_f[5 * QS + j] = noz;
             q_f[6 * QS + j] = w;
             q_info[j] = lx | (ly << 8) | (lz << 16) | ((dcx + 1) << 24) | ((dcy + 1) << 26) |
-                        ((dcz + 1) << 28);
+                        ((dcz + 1) << 28) | (sp_i << 30);
         }
         wq += __popc(qmask);
         if (!REGACC) {
@@ -1412,24 +1471,36 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         if constexpr (PCSBOX) {   // PCS stayers: the warp's boxes, no atomics
             if (__any_sync(0xffffffffu, pstay))
                 deposit_pcs_box(wbox, lx, ly - 4 * (wid & 1), pstay, ox, oy, oz, nox, noy, noz, w,
-                                sp.fac[0], sp.fac[1], sp.fac[2]);
+                                NS == 2 ? tab[sp_i].fac[0] : sp.fac[0],
+                                NS == 2 ? tab[sp_i].fac[1] : sp.fac[1],
+                                NS == 2 ? tab[sp_i].fac[2] : sp.fac[2]);
         }
 
         // ---- write the particle to its column / the exchange --------------
         {   // one store block for stayers (own column front) and in-super-cell
             // movers (destination column back): less code, fewer reconvergence points
             int frame = -1, cell = t;
+            const int Ks = sp_i ? K1 : K;
             if (stay) {
-                frame = fo++;
+                frame = sp_i ? fo1 : fo;
+                fo += sp_i ? 0 : 1;
+                fo1 += sp_i;
             } else if (mover) {
-                const int slot = atomicAdd(&arr[nlc], 1);
-                if (slot < K) { frame = K - 1 - slot; cell = nlc; }
+                const int slot = atomicAdd(&arr[sp_i * kMaxCells + nlc], 1);
+                if (slot < Ks) { frame = Ks - 1 - slot; cell = nlc; }
             }
-            if (frame >= 0 && KWB_IN(frame < K && cell < V)) {
-                const int64_t o = ((int64_t)sc * K + frame) * V + cell;
-                out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
-                out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
-                out.w[o] = w;
+            if (frame >= 0 && KWB_IN(frame < Ks && cell < V)) {
+                const int64_t o = ((int64_t)sc * Ks + frame) * V + cell;
+                if (NS == 2) {
+                    F *const *op = tab[sp_i].out;
+                    op[0][o] = nox; op[1][o] = noy; op[2][o] = noz;
+                    op[3][o] = nux; op[4][o] = nuy; op[5][o] = nuz;
+                    op[6][o] = w;
+                } else {
+                    out.ox[o] = nox; out.oy[o] = noy; out.oz[o] = noz;
+                    out.ux[o] = nux; out.uy[o] = nuy; out.uz[o] = nuz;
+                    out.w[o] = w;
+                }
             }
         }
         const unsigned lm = __ballot_sync(0xffffffffu, leave);
@@ -1445,7 +1516,9 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                     ex.ux[k] = nux; ex.uy[k] = nuy; ex.uz[k] = nuz;
                     ex.w[k] = w;
                     ex.cx[k] = ncx; ex.cy[k] = ncy; ex.cz[k] = ncz;
-                    ex.dest[k] = dest;
+                    // fused species: the destination carries the species
+                    // (shift_kernel: s = dest / n_sc)
+                    ex.dest[k] = dest + sp_i * (g.gx * g.gy * g.gz);
                 } else {
                     atomicAdd(&status[KWB_ST_EXCH_OVERFLOW], 1);
                 }
@@ -1499,21 +1572,19 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             }
         }
     }
-    if (tma_j) fence_proxy_async();   // this thread's J tile writes -> the async proxy
     __syncthreads();
 
-    // ---- flush the J tile: one TMA reduce-add (interior), else coalesced
-    // red.global.add of the non-zero entries ---------------------------------
+    // ---- flush the J tile: coalesced red.global.add of non-zero entries ---
+    // (a TMA reduce-add of the tile needs a 16-byte aligned box start, i.e. a
+    // halo of 4 in x instead of the shape's 2: the wider tile does not fit
+    // the shared-memory budget of 2 CTAs per SM)
     auto jrow = [&](int c, int d, int b) -> F * {   // row (tile z d, tile y b) of J[c]
         if (fp.jpl)
             return (F *)fp.jpl[c * g.nz + wjz[d]] + (int64_t)wjy[b] * g.nx;
         F *dst = (F *)(c == 0 ? fp.J[0] : c == 1 ? fp.J[1] : fp.J[2]);
         return dst + ((int64_t)wjz[d] * g.ny + wjy[b]) * g.nx;
     };
-    if (tma_j) {
-        // the tile's smem must stay valid until the bulk read completes
-        if (t == 0) tma_reduce_add_4d(&tm_j, orgx - H, orgy - H, orgz - H, 0, jt);
-    } else if (sizeof(F) == 4 && (L.jx & 1) == 0) {
+    if (sizeof(F) == 4 && (L.jx & 1) == 0) {
         // x-adjacent pairs with one red.global.add.v2.f32 where the pair is
         // contiguous and 8-byte aligned in J (not across the periodic seam)
         const int total = 3 * L.JV / 2, nth = blockDim.x, jxy = L.jx * L.jy;
@@ -1554,7 +1625,15 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         out.back[col] = nb < K ? nb : K;
         if (fo + nb > K) atomicAdd(&status[KWB_ST_STORE_OVERFLOW], fo + nb - K);
         atomicMax(&s_maxcol, fo + nb);
+        if (NS == 2) {
+            const int nb1 = arr[kMaxCells + t];
+            sb.out.front[col] = fo1;
+            sb.out.back[col] = nb1 < K1 ? nb1 : K1;
+            if (fo1 + nb1 > K1) atomicAdd(&sb.status[KWB_ST_STORE_OVERFLOW], fo1 + nb1 - K1);
+            atomicMax(&s_maxcol1, fo1 + nb1);
+        }
     }
     __syncthreads();
     if (t == 0) atomicMax(&status[KWB_ST_MAX_COUNT], s_maxcol);
+    if (NS == 2 && t == 32) atomicMax(&sb.status[KWB_ST_MAX_COUNT], s_maxcol1);
 }

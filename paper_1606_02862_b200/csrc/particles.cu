@@ -36,35 +36,45 @@ namespace kwb {
 
 // Append leavers to the back of their new column (the cross-super-cell
 // shift, pic/particles.py:316-345).  Slot claims are atomic per column.
-template <typename F>
-__global__ void shift_kernel(StoreT<F> out, ExchT<F> ex, Geo g, int32_t *__restrict__ status) {
+// NS = 2 (species-fused advance): dest = super cell + species * n_sc.
+template <typename F, int NS>
+__global__ void shift_kernel(StoreT<F> out, StoreT<F> out1, ExchT<F> ex, Geo g,
+                             int32_t *__restrict__ status, int32_t *__restrict__ status1) {
     int n = *ex.count;
     if (n > ex.capacity) n = ex.capacity;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&status[KWB_ST_LEAVERS], n);
-    const int V = g.scx * g.scy * g.scz, K = out.frames;
-    int fill_max = 0;   // warp-aggregated: one same-address atomicMax per warp, not per record
+    const int V = g.scx * g.scy * g.scz, n_sc = g.gx * g.gy * g.gz;
+    int fill_max[NS] = {};   // warp-aggregated: one same-address atomicMax per warp, not per record
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int d = ex.dest[i];
+        int d = ex.dest[i];
+        const int s = (NS == 2 && d >= n_sc) ? 1 : 0;
+        d -= s * n_sc;
+        const StoreT<F> &o_ = s ? out1 : out;
+        const int K = o_.frames;
         const int bx = d % g.gx, by = (d / g.gx) % g.gy, bz = d / (g.gx * g.gy);
         const int c = (ex.cx[i] - bx * g.scx) +
                       g.scx * ((ex.cy[i] - by * g.scy) + g.scy * (ex.cz[i] - bz * g.scz));
-        if (!KWB_IN(d >= 0 && d < g.gx * g.gy * g.gz && c >= 0 && c < V)) continue;
+        if (!KWB_IN(d >= 0 && d < n_sc && c >= 0 && c < V)) continue;
         const int64_t colx = (int64_t)d * V + c;
-        const int slot = atomicAdd(&out.back[colx], 1);
-        const int fill = out.front[colx] + slot + 1;
+        const int slot = atomicAdd(&o_.back[colx], 1);
+        const int fill = o_.front[colx] + slot + 1;
         if (fill > K) {
-            atomicSub(&out.back[colx], 1);
-            atomicAdd(&status[KWB_ST_STORE_OVERFLOW], 1);
+            atomicSub(&o_.back[colx], 1);
+            atomicAdd(&(s ? status1 : status)[KWB_ST_STORE_OVERFLOW], 1);
             continue;
         }
-        fill_max = max(fill_max, fill);
+        if (s) fill_max[NS - 1] = max(fill_max[NS - 1], fill);
+        else fill_max[0] = max(fill_max[0], fill);
         const int64_t o = ((int64_t)d * K + (K - 1 - slot)) * V + c;
-        out.ox[o] = ex.ox[i]; out.oy[o] = ex.oy[i]; out.oz[o] = ex.oz[i];
-        out.ux[o] = ex.ux[i]; out.uy[o] = ex.uy[i]; out.uz[o] = ex.uz[i];
-        out.w[o] = ex.w[i];
+        o_.ox[o] = ex.ox[i]; o_.oy[o] = ex.oy[i]; o_.oz[o] = ex.oz[i];
+        o_.ux[o] = ex.ux[i]; o_.uy[o] = ex.uy[i]; o_.uz[o] = ex.uz[i];
+        o_.w[o] = ex.w[i];
     }
-    fill_max = __reduce_max_sync(0xffffffffu, fill_max);
-    if ((threadIdx.x & 31) == 0 && fill_max > 0) atomicMax(&status[KWB_ST_MAX_COUNT], fill_max);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int m = __reduce_max_sync(0xffffffffu, fill_max[s]);
+        if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&(s ? status1 : status)[KWB_ST_MAX_COUNT], m);
+    }
 }
 
 // ---- store load / export / repack ---------------------------------------
@@ -456,15 +466,20 @@ static bool lattice_map(CUtensorMap *m, void *const *ptrs, int n, const kwb_grid
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ>
+static int shift_species2(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,
+                          int32_t *status, kwb_stream_t stream);
+static int sm_count();
+
+// sp / in / out: NS entries; status: NS x KWB_STATUS_WORDS
+template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS>
 static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                           void *const B[3], void *const J[3], void *const *jpl,
                           int32_t *status, cudaStream_t stream) {
     Geo geo = geo_of(*g);
     const int threads = block_threads(g);
-    const size_t smem = adv_layout<F, ORDER>(g->scx, g->scy, g->scz).bytes;
-    auto kern = advance_kernel<F, ORDER, REGACC, SX, SY, SZ>;
+    const size_t smem = adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).bytes;
+    auto kern = advance_kernel<F, ORDER, REGACC, SX, SY, SZ, NS>;
     if (smem > 227 * 1024) {
         kwb_set_error("super cell too large for the shared-memory tiles (%zu B)", smem);
         return KWB_EINVAL;
@@ -477,41 +492,71 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
     if (cudaMemsetAsync(ex->count, 0, sizeof(int32_t), stream) != cudaSuccess)
         return kwb_check_launch("exchange counter reset");
     const int n_sc = g->gx * g->gy * g->gz;
-    // E/B box: the tile (super cell + 1 guard), x padded to 16 bytes; J box:
-    // the J tile (super cell + shape halo) -- float32 J only (TMA reduce-add)
-    CUtensorMap tm_eb, tm_j;
+    // E/B box: the tile (super cell + 1 guard) from a 16-byte aligned x start
+    // (origin - 4 for f32, origin - 2 for f64; csrc/advance.cuh kTmaX0)
+    CUtensorMap tm_eb;
     memset(&tm_eb, 0, sizeof(tm_eb));
-    memset(&tm_j, 0, sizeof(tm_j));
     int tma = 0;
     if (REGACC) {
-        constexpr int H = Shape<ORDER>::H;
-        const cuuint32_t tx = (cuuint32_t)g->scx + 2;
-        const cuuint32_t ebox[4] = {(cuuint32_t)((tx * sizeof(F) + 15) / 16 * 16 / sizeof(F)),
-                                    (cuuint32_t)g->scy + 2, (cuuint32_t)g->scz + 2, 6};
+        const cuuint32_t vec = 16 / sizeof(F), x0 = sizeof(F) == 4 ? 4 : 2;
+        const cuuint32_t need = (cuuint32_t)g->scx + 1 + x0;   // origin - x0 .. origin + scx
+        const cuuint32_t ebox[4] = {(need + vec - 1) / vec * vec, (cuuint32_t)g->scy + 2,
+                                    (cuuint32_t)g->scz + 2, 6};
         void *eb[6] = {E[0], E[1], E[2], B[0], B[1], B[2]};
-        if (ebox[0] <= 256 && ebox[1] <= 256 && lattice_map<F>(&tm_eb, eb, 6, g, ebox))
+        // the box start origin - x0 is 16-byte aligned when scx is a multiple of x0
+        if (g->scx % x0 == 0 && ebox[0] <= 256 && ebox[1] <= 256 && ebox[2] <= 256 &&
+            (size_t)6 * ebox[0] * ebox[1] * ebox[2] * sizeof(F) <=
+                adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).off_arr -
+                    adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).off_qf &&
+            lattice_map<F>(&tm_eb, eb, 6, g, ebox))
             tma |= TMA_EB;
-        const cuuint32_t jbox[4] = {(cuuint32_t)(g->scx + 2 * H), (cuuint32_t)(g->scy + 2 * H),
-                                    (cuuint32_t)(g->scz + 2 * H), 3};
-        if (sizeof(F) == 4 && !jpl && jbox[0] <= 256 && jbox[1] <= 256 &&
-            lattice_map<F>(&tm_j, J, 3, g, jbox))
-            tma |= TMA_J;
+        if (const char *m = getenv("KWB_TMA_MASK")) tma &= atoi(m);   // debugging / A/B
     }
-    kern<<<n_sc, threads, smem, stream>>>(geo, *sp, store_of<F>(*in), store_of<F>(*out),
-                                          exch_of<F>(*ex), fp, status, tm_eb, tm_j, tma);
+    SpeciesB<F> sb;
+    memset(&sb, 0, sizeof(sb));
+    if (NS == 2) {
+        sb.in = store_of<F>(in[1]);
+        sb.out = store_of<F>(out[1]);
+        sb.sp = sp[1];
+        sb.status = status + KWB_STATUS_WORDS;
+    }
+    kern<<<n_sc, threads, smem, stream>>>(geo, sp[0], store_of<F>(in[0]), store_of<F>(out[0]),
+                                          exch_of<F>(*ex), fp, status, tm_eb, tma, sb);
     return kwb_check_launch("advance_kernel");
 }
 
 // Compile-time (8,8,4) super cell (the reference default, every BASELINE
 // config) or a runtime-shaped generic instance.
-template <typename F, int ORDER, bool REGACC>
+template <typename F, int ORDER, bool REGACC, int NS>
 static int dispatch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                             const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                             void *const B[3], void *const J[3], void *const *jpl,
                             int32_t *status, cudaStream_t stream) {
     if (g->scx == 8 && g->scy == 8 && g->scz == 4)
-        return launch_advance<F, ORDER, REGACC, 8, 8, 4>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
-    return launch_advance<F, ORDER, REGACC, 0, 0, 0>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
+        return launch_advance<F, ORDER, REGACC, 8, 8, 4, NS>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
+    return launch_advance<F, ORDER, REGACC, 0, 0, 0, NS>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
+}
+
+template <int NS>
+static int advance_ns(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
+                      const kwb_store *out, const kwb_exchange *ex, void *const E[3],
+                      void *const B[3], void *const J[3], void *const *jpl, int shape_order,
+                      int32_t *status, cudaStream_t s) {
+    if (g->dtype == KWB_F32) {
+        switch (shape_order) {
+            case 1: return dispatch_advance<float, 1, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 2: return dispatch_advance<float, 2, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 3: return dispatch_advance<float, 3, false, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+        }
+    } else {
+        switch (shape_order) {
+            case 1: return dispatch_advance<double, 1, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 2: return dispatch_advance<double, 2, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 3: return dispatch_advance<double, 3, false, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+        }
+    }
+    kwb_set_error("shape_order must be 1 (CIC), 2 (TSC) or 3 (PCS), got %d", shape_order);
+    return KWB_EINVAL;
 }
 
 extern "C" int kwb_particles_advance(const kwb_grid *g, const kwb_species *sp,
@@ -541,22 +586,49 @@ extern "C" int kwb_particles_advance_zslab(const kwb_grid *g, const kwb_species 
         kwb_set_error("advance: input and output stores differ in frames_per_sc");
         return KWB_EINVAL;
     }
-    cudaStream_t s = (cudaStream_t)stream;
-    if (g->dtype == KWB_F32) {
-        switch (shape_order) {
-            case 1: return dispatch_advance<float, 1, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 2: return dispatch_advance<float, 2, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 3: return dispatch_advance<float, 3, false>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-        }
-    } else {
-        switch (shape_order) {
-            case 1: return dispatch_advance<double, 1, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 2: return dispatch_advance<double, 2, true>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 3: return dispatch_advance<double, 3, false>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+    return advance_ns<1>(g, sp, in, out, ex, E, B, J, jpl, shape_order, status,
+                         (cudaStream_t)stream);
+}
+
+// All species of a Simulation in as few launches as possible: two species
+// share one fused launch (lane-level fusion, csrc/advance.cuh SpeciesB);
+// otherwise one launch per species.  The exchange buffer is shared (a fused
+// launch encodes the species in dest, see kwb_particles_shift_species).
+extern "C" int kwb_particles_advance_species(const kwb_grid *g, int32_t n_species,
+                                             const kwb_species *sp, const kwb_store *in,
+                                             const kwb_store *out, const kwb_exchange *ex,
+                                             void *const E[3], void *const B[3],
+                                             void *const J[3], void *const *j_planes,
+                                             int shape_order, int32_t *status,
+                                             kwb_stream_t stream) {
+    int rc = check_grid(g);
+    if (rc) return rc;
+    if (n_species < 1 || !sp || !in || !out || !ex || !ex->count || !status || !E || !B || !J) {
+        kwb_set_error("advance_species: NULL argument or no species");
+        return KWB_EINVAL;
+    }
+    for (int i = 0; i < n_species; ++i) {
+        if ((rc = check_store(in + i, "input")) || (rc = check_store(out + i, "output"))) return rc;
+        if (out[i].frames_per_sc != in[i].frames_per_sc) {
+            kwb_set_error("advance_species: input and output stores differ in frames_per_sc");
+            return KWB_EINVAL;
         }
     }
-    kwb_set_error("shape_order must be 1 (CIC), 2 (TSC) or 3 (PCS), got %d", shape_order);
-    return KWB_EINVAL;
+    if (n_species == 2 && !getenv("KWB_NO_SPECIES_FUSION")) {
+        if ((rc = advance_ns<2>(g, sp, in, out, ex, E, B, J, j_planes, shape_order, status,
+                                (cudaStream_t)stream)))
+            return rc;
+        return shift_species2(g, out, ex, status, stream);
+    }
+    for (int i = 0; i < n_species; ++i) {
+        rc = kwb_particles_advance_zslab(g, sp + i, in + i, out + i, ex, E, B, J, j_planes,
+                                         shape_order, status + i * KWB_STATUS_WORDS, stream);
+        if (rc) return rc;
+        // the species of a per-species launch are shifted right after it
+        if ((rc = kwb_particles_shift(g, out + i, ex, status + i * KWB_STATUS_WORDS, stream)))
+            return rc;
+    }
+    return KWB_OK;
 }
 
 static int sm_count() {
@@ -590,9 +662,28 @@ extern "C" int kwb_particles_shift(const kwb_grid *g, const kwb_store *out,
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = sm_count() * 4;
     if (g->dtype == KWB_F32)
-        shift_kernel<float><<<blocks, 256, 0, s>>>(store_of<float>(*out), exch_of<float>(*ex), geo, status);
+        shift_kernel<float, 1><<<blocks, 256, 0, s>>>(store_of<float>(*out), store_of<float>(*out),
+                                                      exch_of<float>(*ex), geo, status, status);
     else
-        shift_kernel<double><<<blocks, 256, 0, s>>>(store_of<double>(*out), exch_of<double>(*ex), geo, status);
+        shift_kernel<double, 1><<<blocks, 256, 0, s>>>(store_of<double>(*out), store_of<double>(*out),
+                                                       exch_of<double>(*ex), geo, status, status);
+    return kwb_check_launch("shift_kernel");
+}
+
+// Shift after a species-fused advance (kwb_particles_advance_species).
+static int shift_species2(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,
+                          int32_t *status, kwb_stream_t stream) {
+    Geo geo = geo_of(*g);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = sm_count() * 4;
+    if (g->dtype == KWB_F32)
+        shift_kernel<float, 2><<<blocks, 256, 0, s>>>(store_of<float>(out[0]), store_of<float>(out[1]),
+                                                      exch_of<float>(*ex), geo, status,
+                                                      status + KWB_STATUS_WORDS);
+    else
+        shift_kernel<double, 2><<<blocks, 256, 0, s>>>(store_of<double>(out[0]), store_of<double>(out[1]),
+                                                       exch_of<double>(*ex), geo, status,
+                                                       status + KWB_STATUS_WORDS);
     return kwb_check_launch("shift_kernel");
 }
 

@@ -151,6 +151,9 @@ class Simulation:
         self.tile_shape = tuple(sc[a] + 2 * hw for a in range(3))
         self._grid = _grid_struct(p)
         self._species = [_species_struct(p, sp) for sp in p.species]
+        # one particle-phase call for all species (two species: one fused
+        # launch); False: the reference's per-species launches
+        self.fuse_species = os.environ.get("KWB_PER_SPECIES", "0") != "1"
         self._status = torch.zeros((len(p.species), _lib.STATUS_WORDS), dtype=torch.int32,
                                    device=self.device)
         self._status_host = torch.zeros_like(self._status, device="cpu").pin_memory()
@@ -192,7 +195,8 @@ class Simulation:
         return _lib.ptr3([self.fields.storage(n) for n in ("Jx", "Jy", "Jz")])
 
     def _exchange_buffer(self) -> _Exchange:
-        need = max(st.loaded for st in self.stores)
+        # species-fused launches share the buffer between the species
+        need = sum(st.loaded for st in self.stores)
         cap = int(math.ceil(EXCHANGE_FRACTION * need)) + 65536
         if self._exchange is None or self._exchange.capacity < min(cap, need + 65536):
             self._exchange = _Exchange(min(cap, need + 65536), self.stores[0].tdtype, self.device)
@@ -312,6 +316,21 @@ class Simulation:
                   self._status.data_ptr(), self._status.numel(), stream)
         ex = self._exchange_buffer()
         jpl = getattr(self, "_jplanes", None)
+        if self.fuse_species:
+            # every species' advance + shift in one call: two species share
+            # one fused launch (kwb_particles_advance_species)
+            n = len(self.stores)
+            ins = (_lib.StoreC * n)(*[st.current.cstruct() for st in self.stores])
+            outs = (_lib.StoreC * n)(*[st.spare().cstruct() for st in self.stores])
+            sps = (_lib.SpeciesC * n)(*self._species)
+            with _nvtx("particles[all species]"):
+                _lib.call("kwb_particles_advance_species", g, n, sps, ins, outs,
+                          ctypes.byref(ex.cstruct), E, B, J,
+                          jpl.data_ptr() if jpl is not None else None,
+                          self.shape_order, self._status.data_ptr(), stream)
+            for st in self.stores:
+                st.swap()
+            return
         for i, st in enumerate(self.stores):
             src, dst = st.current, st.spare()
             with _nvtx(f"advance[{i}]"):
