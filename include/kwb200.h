@@ -161,11 +161,14 @@ int kwb_fields_faraday_half(const kwb_grid *g, void *const E[3], void *const B[3
 int kwb_fields_ampere(const kwb_grid *g, void *const E[3], void *const B[3],
                       void *const J[3], double dt, kwb_stream_t stream);
 
-/* The whole particle phase of a step for all species of a Simulation
- * (advance + super-cell shift; the reference launches its four particle
- * kernels per species, pic/sim.py:141-163): two species run in ONE fused
- * advance launch (lane-level species fusion) and one shift; otherwise one
- * advance + shift per species.  sp/in/out: n_species entries; status:
+/* The particle phase of a step for all species of a Simulation (the
+ * reference launches its particle kernels per species, pic/sim.py:141-163):
+ * kwb_particles_advance_species advances every species -- two species in
+ * ONE fused launch (lane-level species fusion), otherwise one launch per
+ * species, all appending their super-cell leavers to the one exchange buffer
+ * (dest = super cell + species * n_super_cells) -- and
+ * kwb_particles_shift_species then appends every leaver to its species'
+ * store in one launch.  sp/in/out: n_species (<= 4) entries; status:
  * n_species x KWB_STATUS_WORDS; j_planes as kwb_particles_advance_zslab
  * (NULL: plain J). */
 int kwb_particles_advance_species(const kwb_grid *g, int32_t n_species, const kwb_species *sp,
@@ -173,6 +176,8 @@ int kwb_particles_advance_species(const kwb_grid *g, int32_t n_species, const kw
                                   const kwb_exchange *ex, void *const E[3], void *const B[3],
                                   void *const J[3], void *const *j_planes, int shape_order,
                                   int32_t *status, kwb_stream_t stream);
+int kwb_particles_shift_species(const kwb_grid *g, int32_t n_species, const kwb_store *out,
+                                const kwb_exchange *ex, int32_t *status, kwb_stream_t stream);
 
 /* Multi-GPU plumbing for the fused z-slab halo (pic/decomp.py): enable
  * access from the CURRENT device to peer_device (already enabled = OK), and

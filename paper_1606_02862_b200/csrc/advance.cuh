@@ -1034,7 +1034,7 @@ template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS>
 __global__ void __launch_bounds__(kMaxCells, AdvCfg<F, ORDER>::kMinBlocks)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
                int32_t *__restrict__ status, const __grid_constant__ CUtensorMap tm_eb, int tma,
-               SpeciesB<F> sb) {
+               SpeciesB<F> sb, int sp0) {
     static_assert(NS == 1 || NS == 2, "one or two species per launch");
     constexpr int H = Shape<ORDER>::H;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1518,7 +1518,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
                     ex.cx[k] = ncx; ex.cy[k] = ncy; ex.cz[k] = ncz;
                     // fused species: the destination carries the species
                     // (shift_kernel: s = dest / n_sc)
-                    ex.dest[k] = dest + sp_i * (g.gx * g.gy * g.gz);
+                    ex.dest[k] = dest + (sp0 + sp_i) * (g.gx * g.gy * g.gz);
                 } else {
                     atomicAdd(&status[KWB_ST_EXCH_OVERFLOW], 1);
                 }

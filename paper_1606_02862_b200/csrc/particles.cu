@@ -36,20 +36,26 @@ namespace kwb {
 
 // Append leavers to the back of their new column (the cross-super-cell
 // shift, pic/particles.py:316-345).  Slot claims are atomic per column.
-// NS = 2 (species-fused advance): dest = super cell + species * n_sc.
-template <typename F, int NS>
-__global__ void shift_kernel(StoreT<F> out, StoreT<F> out1, ExchT<F> ex, Geo g,
-                             int32_t *__restrict__ status, int32_t *__restrict__ status1) {
+// All species of a step at once: dest = super cell + species * n_sc.
+constexpr int kMaxSpecies = 4;
+template <typename F>
+struct ShiftOut {
+    StoreT<F> out[kMaxSpecies];
+};
+template <typename F>
+__global__ void shift_kernel(ShiftOut<F> so, int n_species, ExchT<F> ex, Geo g,
+                             int32_t *__restrict__ status) {
     int n = *ex.count;
     if (n > ex.capacity) n = ex.capacity;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&status[KWB_ST_LEAVERS], n);
     const int V = g.scx * g.scy * g.scz, n_sc = g.gx * g.gy * g.gz;
-    int fill_max[NS] = {};   // warp-aggregated: one same-address atomicMax per warp, not per record
+    int fill_max[kMaxSpecies] = {};   // warp-aggregated: one atomicMax per warp and species
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         int d = ex.dest[i];
-        const int s = (NS == 2 && d >= n_sc) ? 1 : 0;
+        const int s = d / n_sc;
         d -= s * n_sc;
-        const StoreT<F> &o_ = s ? out1 : out;
+        if (!KWB_IN(s >= 0 && s < n_species)) continue;
+        const StoreT<F> &o_ = so.out[s];
         const int K = o_.frames;
         const int bx = d % g.gx, by = (d / g.gx) % g.gy, bz = d / (g.gx * g.gy);
         const int c = (ex.cx[i] - bx * g.scx) +
@@ -60,20 +66,22 @@ __global__ void shift_kernel(StoreT<F> out, StoreT<F> out1, ExchT<F> ex, Geo g,
         const int fill = o_.front[colx] + slot + 1;
         if (fill > K) {
             atomicSub(&o_.back[colx], 1);
-            atomicAdd(&(s ? status1 : status)[KWB_ST_STORE_OVERFLOW], 1);
+            atomicAdd(&status[s * KWB_STATUS_WORDS + KWB_ST_STORE_OVERFLOW], 1);
             continue;
         }
-        if (s) fill_max[NS - 1] = max(fill_max[NS - 1], fill);
-        else fill_max[0] = max(fill_max[0], fill);
+#pragma unroll
+        for (int k = 0; k < kMaxSpecies; ++k)
+            if (k == s) fill_max[k] = max(fill_max[k], fill);
         const int64_t o = ((int64_t)d * K + (K - 1 - slot)) * V + c;
         o_.ox[o] = ex.ox[i]; o_.oy[o] = ex.oy[i]; o_.oz[o] = ex.oz[i];
         o_.ux[o] = ex.ux[i]; o_.uy[o] = ex.uy[i]; o_.uz[o] = ex.uz[i];
         o_.w[o] = ex.w[i];
     }
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        const int m = __reduce_max_sync(0xffffffffu, fill_max[s]);
-        if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&(s ? status1 : status)[KWB_ST_MAX_COUNT], m);
+    for (int k = 0; k < kMaxSpecies; ++k) {
+        const int m = __reduce_max_sync(0xffffffffu, fill_max[k]);
+        if ((threadIdx.x & 31) == 0 && m > 0 && k < n_species)
+            atomicMax(&status[k * KWB_STATUS_WORDS + KWB_ST_MAX_COUNT], m);
     }
 }
 
@@ -466,16 +474,29 @@ static bool lattice_map(CUtensorMap *m, void *const *ptrs, int n, const kwb_grid
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int shift_species2(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,
-                          int32_t *status, kwb_stream_t stream);
 static int sm_count();
+template <typename F>
+static int shift_launch(const kwb_grid *g, int n, const kwb_store *out, const kwb_exchange *ex,
+                        int32_t *status, cudaStream_t s) {
+    ShiftOut<F> so;
+    memset(&so, 0, sizeof(so));
+    for (int i = 0; i < n; ++i) so.out[i] = store_of<F>(out[i]);
+    shift_kernel<F><<<sm_count() * 4, 256, 0, s>>>(so, n, exch_of<F>(*ex), geo_of(*g), status);
+    return kwb_check_launch("shift_kernel");
+}
+static int shift_all(const kwb_grid *g, int n, const kwb_store *out, const kwb_exchange *ex,
+                     int32_t *status, kwb_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    return g->dtype == KWB_F32 ? shift_launch<float>(g, n, out, ex, status, s)
+                               : shift_launch<double>(g, n, out, ex, status, s);
+}
 
 // sp / in / out: NS entries; status: NS x KWB_STATUS_WORDS
 template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS>
 static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                           void *const B[3], void *const J[3], void *const *jpl,
-                          int32_t *status, cudaStream_t stream) {
+                          int32_t *status, cudaStream_t stream, int sp0, bool reset) {
     Geo geo = geo_of(*g);
     const int threads = block_threads(g);
     const size_t smem = adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).bytes;
@@ -489,7 +510,7 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
     FieldPtrs fp;
     for (int c = 0; c < 3; ++c) { fp.E[c] = E[c]; fp.B[c] = B[c]; fp.J[c] = J[c]; }
     fp.jpl = jpl;
-    if (cudaMemsetAsync(ex->count, 0, sizeof(int32_t), stream) != cudaSuccess)
+    if (reset && cudaMemsetAsync(ex->count, 0, sizeof(int32_t), stream) != cudaSuccess)
         return kwb_check_launch("exchange counter reset");
     const int n_sc = g->gx * g->gy * g->gz;
     // E/B box: the tile (super cell + 1 guard) from a 16-byte aligned x start
@@ -521,7 +542,7 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
         sb.status = status + KWB_STATUS_WORDS;
     }
     kern<<<n_sc, threads, smem, stream>>>(geo, sp[0], store_of<F>(in[0]), store_of<F>(out[0]),
-                                          exch_of<F>(*ex), fp, status, tm_eb, tma, sb);
+                                          exch_of<F>(*ex), fp, status, tm_eb, tma, sb, sp0);
     return kwb_check_launch("advance_kernel");
 }
 
@@ -531,28 +552,30 @@ template <typename F, int ORDER, bool REGACC, int NS>
 static int dispatch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                             const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                             void *const B[3], void *const J[3], void *const *jpl,
-                            int32_t *status, cudaStream_t stream) {
+                            int32_t *status, cudaStream_t stream, int sp0, bool reset) {
     if (g->scx == 8 && g->scy == 8 && g->scz == 4)
-        return launch_advance<F, ORDER, REGACC, 8, 8, 4, NS>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
-    return launch_advance<F, ORDER, REGACC, 0, 0, 0, NS>(g, sp, in, out, ex, E, B, J, jpl, status, stream);
+        return launch_advance<F, ORDER, REGACC, 8, 8, 4, NS>(g, sp, in, out, ex, E, B, J, jpl,
+                                                             status, stream, sp0, reset);
+    return launch_advance<F, ORDER, REGACC, 0, 0, 0, NS>(g, sp, in, out, ex, E, B, J, jpl, status,
+                                                         stream, sp0, reset);
 }
 
 template <int NS>
 static int advance_ns(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                       const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                       void *const B[3], void *const J[3], void *const *jpl, int shape_order,
-                      int32_t *status, cudaStream_t s) {
+                      int32_t *status, cudaStream_t s, int sp0 = 0, bool reset = true) {
     if (g->dtype == KWB_F32) {
         switch (shape_order) {
-            case 1: return dispatch_advance<float, 1, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 2: return dispatch_advance<float, 2, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 3: return dispatch_advance<float, 3, false, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 1: return dispatch_advance<float, 1, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s, sp0, reset);
+            case 2: return dispatch_advance<float, 2, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s, sp0, reset);
+            case 3: return dispatch_advance<float, 3, false, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s, sp0, reset);
         }
     } else {
         switch (shape_order) {
-            case 1: return dispatch_advance<double, 1, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 2: return dispatch_advance<double, 2, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
-            case 3: return dispatch_advance<double, 3, false, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s);
+            case 1: return dispatch_advance<double, 1, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s, sp0, reset);
+            case 2: return dispatch_advance<double, 2, true, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s, sp0, reset);
+            case 3: return dispatch_advance<double, 3, false, NS>(g, sp, in, out, ex, E, B, J, jpl, status, s, sp0, reset);
         }
     }
     kwb_set_error("shape_order must be 1 (CIC), 2 (TSC) or 3 (PCS), got %d", shape_order);
@@ -614,19 +637,19 @@ extern "C" int kwb_particles_advance_species(const kwb_grid *g, int32_t n_specie
             return KWB_EINVAL;
         }
     }
-    if (n_species == 2 && !getenv("KWB_NO_SPECIES_FUSION")) {
-        if ((rc = advance_ns<2>(g, sp, in, out, ex, E, B, J, j_planes, shape_order, status,
-                                (cudaStream_t)stream)))
-            return rc;
-        return shift_species2(g, out, ex, status, stream);
+    if (n_species > kMaxSpecies) {
+        kwb_set_error("advance_species: at most %d species", kMaxSpecies);
+        return KWB_EINVAL;
     }
+    if (n_species == 2 && !getenv("KWB_NO_SPECIES_FUSION"))
+        return advance_ns<2>(g, sp, in, out, ex, E, B, J, j_planes, shape_order, status,
+                             (cudaStream_t)stream);
+    // one launch per species, all appending their leavers to the one
+    // exchange buffer (dest carries the species; counter reset once)
     for (int i = 0; i < n_species; ++i) {
-        rc = kwb_particles_advance_zslab(g, sp + i, in + i, out + i, ex, E, B, J, j_planes,
-                                         shape_order, status + i * KWB_STATUS_WORDS, stream);
+        rc = advance_ns<1>(g, sp + i, in + i, out + i, ex, E, B, J, j_planes, shape_order,
+                           status + i * KWB_STATUS_WORDS, (cudaStream_t)stream, i, i == 0);
         if (rc) return rc;
-        // the species of a per-species launch are shifted right after it
-        if ((rc = kwb_particles_shift(g, out + i, ex, status + i * KWB_STATUS_WORDS, stream)))
-            return rc;
     }
     return KWB_OK;
 }
@@ -658,33 +681,22 @@ extern "C" int kwb_particles_shift(const kwb_grid *g, const kwb_store *out,
         kwb_set_error("shift: NULL argument");
         return KWB_EINVAL;
     }
-    Geo geo = geo_of(*g);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int blocks = sm_count() * 4;
-    if (g->dtype == KWB_F32)
-        shift_kernel<float, 1><<<blocks, 256, 0, s>>>(store_of<float>(*out), store_of<float>(*out),
-                                                      exch_of<float>(*ex), geo, status, status);
-    else
-        shift_kernel<double, 1><<<blocks, 256, 0, s>>>(store_of<double>(*out), store_of<double>(*out),
-                                                       exch_of<double>(*ex), geo, status, status);
-    return kwb_check_launch("shift_kernel");
+    return shift_all(g, 1, out, ex, status, stream);
 }
 
-// Shift after a species-fused advance (kwb_particles_advance_species).
-static int shift_species2(const kwb_grid *g, const kwb_store *out, const kwb_exchange *ex,
-                          int32_t *status, kwb_stream_t stream) {
-    Geo geo = geo_of(*g);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int blocks = sm_count() * 4;
-    if (g->dtype == KWB_F32)
-        shift_kernel<float, 2><<<blocks, 256, 0, s>>>(store_of<float>(out[0]), store_of<float>(out[1]),
-                                                      exch_of<float>(*ex), geo, status,
-                                                      status + KWB_STATUS_WORDS);
-    else
-        shift_kernel<double, 2><<<blocks, 256, 0, s>>>(store_of<double>(out[0]), store_of<double>(out[1]),
-                                                       exch_of<double>(*ex), geo, status,
-                                                       status + KWB_STATUS_WORDS);
-    return kwb_check_launch("shift_kernel");
+// The shift of every species after kwb_particles_advance_species.
+extern "C" int kwb_particles_shift_species(const kwb_grid *g, int32_t n_species,
+                                           const kwb_store *out, const kwb_exchange *ex,
+                                           int32_t *status, kwb_stream_t stream) {
+    int rc = check_grid(g);
+    if (rc) return rc;
+    if (n_species < 1 || n_species > kMaxSpecies || !out || !ex || !ex->count || !status) {
+        kwb_set_error("shift_species: NULL argument or 1..%d species", kMaxSpecies);
+        return KWB_EINVAL;
+    }
+    for (int i = 0; i < n_species; ++i)
+        if ((rc = check_store(out + i, "output"))) return rc;
+    return shift_all(g, n_species, out, ex, status, stream);
 }
 
 static int store_load(const kwb_grid *g, const kwb_store *st, int64_t n, const int64_t *n_dev,

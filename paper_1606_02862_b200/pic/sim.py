@@ -153,7 +153,7 @@ class Simulation:
         self._species = [_species_struct(p, sp) for sp in p.species]
         # one particle-phase call for all species (two species: one fused
         # launch); False: the reference's per-species launches
-        self.fuse_species = os.environ.get("KWB_PER_SPECIES", "0") != "1"
+        self.fuse_species = os.environ.get("KWB_PER_SPECIES", "0") != "1" and len(p.species) <= 4
         self._status = torch.zeros((len(p.species), _lib.STATUS_WORDS), dtype=torch.int32,
                                    device=self.device)
         self._status_host = torch.zeros_like(self._status, device="cpu").pin_memory()
@@ -323,11 +323,14 @@ class Simulation:
             ins = (_lib.StoreC * n)(*[st.current.cstruct() for st in self.stores])
             outs = (_lib.StoreC * n)(*[st.spare().cstruct() for st in self.stores])
             sps = (_lib.SpeciesC * n)(*self._species)
-            with _nvtx("particles[all species]"):
+            with _nvtx("advance[all species]"):
                 _lib.call("kwb_particles_advance_species", g, n, sps, ins, outs,
                           ctypes.byref(ex.cstruct), E, B, J,
                           jpl.data_ptr() if jpl is not None else None,
                           self.shape_order, self._status.data_ptr(), stream)
+            with _nvtx("shift[all species]"):
+                _lib.call("kwb_particles_shift_species", g, n, outs, ctypes.byref(ex.cstruct),
+                          self._status.data_ptr(), stream)
             for st in self.stores:
                 st.swap()
             return

@@ -19,7 +19,9 @@ def main(path):
         j = [r for r in rs if r["field"].startswith("J")]
         eb = [r for r in rs if r["field"][0] in "EB"]
         other = [r for r in rs if r not in j and r not in eb]
-        w = max(rs, key=lambda r: r["err"] / r["tol"] if r["tol"] else 0.0)
+        def ratio(r):
+            return r["err"] / r["tol"] if r["tol"] else (0.0 if r["err"] == 0 else float("inf"))
+        w = max(rs, key=ratio)
         fj = f"{max(r['err'] for r in j):.2e}" if j else "-"
         feb = f"{max(r['err'] for r in eb):.2e}" if eb else "-"
         if other and not j:
@@ -27,7 +29,7 @@ def main(path):
         sp = max((r.get("spread", 0.0) for r in j), default=0.0)
         tol = sorted({r["tol"] for r in rs})
         tols = "/".join(f"{t:.1e}" for t in tol)
-        print(f"| {case} | {kind} | {fj} | {feb} | {sp:.1e} | {tols} | {w['err'] / w['tol']:.2f} |")
+        print(f"| {case} | {kind} | {fj} | {feb} | {sp:.1e} | {tols} | {ratio(w):.2f} |")
 
 
 if __name__ == "__main__":
