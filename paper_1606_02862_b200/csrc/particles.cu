@@ -641,7 +641,13 @@ extern "C" int kwb_particles_advance_species(const kwb_grid *g, int32_t n_specie
         kwb_set_error("advance_species: at most %d species", kMaxSpecies);
         return KWB_EINVAL;
     }
-    if (n_species == 2 && !getenv("KWB_NO_SPECIES_FUSION"))
+    // The species-fused launch (lane-level fusion, NS = 2) is opt-in: on C2
+    // it issues as many warp instructions as the two per-species launches
+    // (+1.5 %: the species selects eat the lane-balance gain, active lanes
+    // 25.6 -> 26.4 of 32) and stalls more (7.8 vs 6.7 cycles per issue:
+    // 9 spilled registers in the hot loop, L1 is ~3 KB next to 2 x 112 KB of
+    // shared memory): 8.14 ms vs 2 x 3.48 ms (ncu, tools/gpurun/r02i_ncu.sh).
+    if (n_species == 2 && getenv("KWB_SPECIES_FUSION") && getenv("KWB_SPECIES_FUSION")[0] == '1')
         return advance_ns<2>(g, sp, in, out, ex, E, B, J, j_planes, shape_order, status,
                              (cudaStream_t)stream);
     // one launch per species, all appending their leavers to the one
