@@ -56,7 +56,7 @@ constexpr int kWarps = kMaxCells / 32;
 #endif
 constexpr int kWarpQ = KWB_WARPQ;         // crossing-particle queue entries per warp
 #ifndef KWB_WARPQ_PCS
-#define KWB_WARPQ_PCS 64
+#define KWB_WARPQ_PCS 32   // 64 with the closing-edge boxes is 116 KB: 1 CTA per SM
 #endif
 #ifndef KWB_MIN_BLOCKS
 #define KWB_MIN_BLOCKS 2
@@ -808,8 +808,9 @@ __device__ __forceinline__ int regacc_offset(int c, int ja, int j1, int j2, int 
 // fastest, 12 x 8 x 5 per component at 0 / 480 / 960.
 // One group: all loads, then all stores (entries of a group never alias
 // across the warp's lanes), so the N read-add-writes overlap.
+// entry i of the group gets p * T[i] (one FFMA at the read-modify-write)
 template <int N>
-__device__ __forceinline__ void box_group(float *b, int stride, const float (&v)[N],
+__device__ __forceinline__ void box_group(float *b, int stride, float p, const float (&T)[N],
                                           const float *box = nullptr) {
 #ifdef KWB_CHECKS
     if (box && !KWB_IN(b >= box && b + (N - 1) * stride < box + kBoxFloats)) return;
@@ -821,8 +822,8 @@ __device__ __forceinline__ void box_group(float *b, int stride, const float (&v)
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o[i]) : "r"(a + 4u * i * stride) : "memory");
 #pragma unroll
     for (int i = 0; i < N; ++i)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u * i * stride), "f"(__fadd_rn(o[i], v[i]))
-                     : "memory");
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u * i * stride),
+                     "f"(__fmaf_rn(p, T[i], o[i])) : "memory");
 #ifndef KWB_EXP_NO_BOX_SYNCWARP   // negative control of the race test (tools/gpurun/r02f.sh)
     __syncwarp();   // measured: without it lanes lose updates (tests/test_gpu_dense.py)
 #endif
@@ -888,10 +889,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
             float pa[5] = {P[0][0], P[0][1], P[0][2], P[0][3], P[0][4]};
 #pragma unroll 1
             for (int ja = 0; ja < 5; ++ja) {
-                float v[5];
-#pragma unroll
-                for (int j2 = 0; j2 < 5; ++j2) v[j2] = pa[0] * T[j2];
-                box_group<5>(b + ja, 96, v, box);
+                box_group<5>(b + ja, 96, pa[0], T, box);
                 pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3]; pa[3] = pa[4];
             }
             b += 12;
@@ -918,10 +916,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
             float pa[5] = {P[1][0], P[1][1], P[1][2], P[1][3], P[1][4]};
 #pragma unroll 1
             for (int ja = 0; ja < 5; ++ja) {
-                float v[5];
-#pragma unroll
-                for (int j1 = 0; j1 < 5; ++j1) v[j1] = pa[0] * T[j1];
-                box_group<5>(b + 12 * ja, 96, v, box);
+                box_group<5>(b + 12 * ja, 96, pa[0], T, box);
                 pa[0] = pa[1]; pa[1] = pa[2]; pa[2] = pa[3]; pa[3] = pa[4];
             }
             b += 1;
@@ -948,10 +943,7 @@ __device__ __forceinline__ void deposit_pcs_box(float *__restrict__ box, int rx,
 #pragma unroll 1
             for (int j2 = 0; j2 < 5; ++j2) {
                 const float T = uu * y0[0] + vv * y1[0];
-                float v[5];
-#pragma unroll
-                for (int ja = 0; ja < 5; ++ja) v[ja] = P[2][ja] * T;
-                box_group<5>(b + 12 * j2, 96, v, box);
+                box_group<5>(b + 12 * j2, 96, T, P[2], box);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) { y0[j] = y0[j + 1]; y1[j] = y1[j + 1]; }
             }
@@ -1447,6 +1439,11 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
         // ---- crossing particles -> this warp's queue (no atomics) ---------
         const unsigned qmask = __ballot_sync(0xffffffffu, queue);
+        if (!REGACC && wq + __popc(qmask) > kQ) {   // PCS ring full: drain what it holds
+            drain_queue();
+            qh = (qh + wq) & (kQ - 1);
+            wq = 0;
+        }
         if (queue && KWB_IN(qidx(wq + __popc(qmask & ((1u << lane) - 1u))) < kQ)) {
             const int j = qidx(wq + __popc(qmask & ((1u << lane) - 1u)));
             q_f[0 * QS + j] = ox; q_f[1 * QS + j] = oy; q_f[2 * QS + j] = oz;

@@ -55,7 +55,10 @@ __global__ void shift_kernel(ShiftOut<F> so, int n_species, ExchT<F> ex, Geo g,
         const int s = d / n_sc;
         d -= s * n_sc;
         if (!KWB_IN(s >= 0 && s < n_species)) continue;
-        const StoreT<F> &o_ = so.out[s];
+        // compile-time indices: a runtime index into the parameter array
+        // would copy it to local memory
+        const StoreT<F> o_ = s == 0 ? so.out[0] : s == 1 ? so.out[1] : s == 2 ? so.out[2]
+                                                                      : so.out[kMaxSpecies - 1];
         const int K = o_.frames;
         const int bx = d % g.gx, by = (d / g.gx) % g.gy, bz = d / (g.gx * g.gy);
         const int c = (ex.cx[i] - bx * g.scx) +

@@ -27,6 +27,7 @@ def main():
     import paper_1606_02862_b200.pic.sim as simmod
     p, seed = bench.make_params(a.config)
     sim = init_khi(p, seed=seed, validate=False, rng="device")
+    sim.use_graphs = False   # direct launches: a replayed graph hides them from the events
     stream = torch.cuda.current_stream()
     evs = []
     orig = _lib.call
