@@ -9,6 +9,12 @@
  *                             DepositKernel (+ ATOMICS.add_dense)
  *                             pic/kernels.py:341-412, kw/atomics.py:147-163
  *   kwb_particles_shift    <- migrate_particles   pic/particles.py:316-345
+ *   kwb_particles_advance_species / kwb_particles_shift_species
+ *                          <- the per-species particle loop of Simulation.step
+ *                             pic/sim.py:141-163 (all species, one shift)
+ *   kwb_zero_step          <- J[:] = 0            pic/sim.py:138-140
+ *   kwb_fields_faraday_half / kwb_fields_ampere also serve the host helpers
+ *                             yee_update_b / yee_update_e  pic/fields.py:127-143
  *   kwb_fields_faraday_half<- FaradayHalfKernel   pic/kernels.py:415-431
  *   kwb_fields_ampere      <- AmpereKernel        pic/kernels.py:434-450
  *   kwb_fields_gather      <- gather_fields       pic/fields.py:95-118
