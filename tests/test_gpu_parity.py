@@ -301,3 +301,82 @@ def test_field_helpers_gather_and_yee(dtype):
             assert np.asarray(g_, dtype=dtype).tobytes() == w_.tobytes()
     e1, b1 = gather_fields(f, ps[0])
     assert e1.shape == (3,) and b1.shape == (3,)
+
+
+@pytest.mark.parametrize("mode", ["fused", "per_species_calls", "shared_exchange"])
+def test_species_paths_agree_with_oracle(mode, monkeypatch):
+    """The three particle-phase paths: two species in one fused launch
+    (KWB_SPECIES_FUSION=1), the reference's per-species advance + shift
+    calls (KWB_PER_SPECIES=1), and per-species launches sharing one
+    exchange buffer with one shift for all species (default).  Teacher
+    forced from the oracle's evolved state of a hot e/ion plasma: particles
+    bitwise, fields within the bars."""
+    monkeypatch.setenv("KWB_SPECIES_FUSION", "1" if mode == "fused" else "0")
+    monkeypatch.setenv("KWB_PER_SPECIES", "1" if mode == "per_species_calls" else "0")
+    meta, _ = load_case("eion_f32")
+    gpu, orc = make_pair(meta, validate=False)
+    assert gpu.fuse_species == (mode != "per_species_calls")
+    orc.run(2)
+    gpu.load_state(fields={n: getattr(orc.fields, n) for n in FIELDS9},
+                   particles=[st.packed() for st in orc.stores])
+    spread = order_spread(orc)
+    gpu.step()
+    orc.step()
+    for gs, os_ in zip(gpu.stores, orc.stores):
+        assert_particles_bitwise(gs, os_)
+    check_fields(f"eion_f32:{mode}", gpu.fields, lambda n: getattr(orc.fields, n),
+                 TOL_1STEP[np.dtype(np.float32)], spread=spread)
+
+
+def test_three_species_share_one_exchange_buffer():
+    """Three species (more than the fused launch takes): one advance launch
+    per species into ONE exchange buffer (dest = super cell + species x
+    n_super_cells) and one shift launch that returns every leaver to its own
+    species' store -- against the oracle, hot plasma (many leavers)."""
+    from oracle.pic import OracleSim
+    from paper_1606_02862_b200.pic import SimParams, Simulation, Species
+    sp = (Species("e", -1.0, 1.0, 0.25), Species("p", 1.0, 4.0, 0.25), Species("x", -2.0, 9.0, 0.5))
+    p = SimParams(cells=(16, 16, 8), species=sp, dtype=np.float32)
+    gpu = Simulation(p, validate=True)
+    orc = OracleSim(p, validate=True, shape_order=2, threads=2)
+    rng = np.random.default_rng(41)
+    recs = []
+    for _ in sp:
+        n = 3000
+        recs.append(dict(cx=rng.integers(0, 16, n).astype(np.int32), cy=rng.integers(0, 16, n).astype(np.int32),
+                         cz=rng.integers(0, 8, n).astype(np.int32),
+                         ox=rng.random(n).astype(np.float32), oy=rng.random(n).astype(np.float32),
+                         oz=rng.random(n).astype(np.float32),
+                         ux=(0.6 * rng.standard_normal(n)).astype(np.float32),
+                         uy=(0.6 * rng.standard_normal(n)).astype(np.float32),
+                         uz=(0.6 * rng.standard_normal(n)).astype(np.float32),
+                         w=np.full(n, 0.25, np.float32)))
+    gpu.load_state(particles=recs)
+    for st, rec in zip(orc.stores, recs):
+        scx, scy, scz = st.super_cell
+        gx, gy, _ = st.sc_grid
+        scid = rec["cx"] // scx + gx * (rec["cy"] // scy + gy * (rec["cz"] // scz))
+        o = np.argsort(scid, kind="stable")
+        st.load_packed(scid[o], {k: np.asarray(v)[o] for k, v in rec.items()})
+    spread = order_spread(orc)
+    gpu.step()
+    orc.step()
+    for gs, os_ in zip(gpu.stores, orc.stores):
+        assert_particles_bitwise(gs, os_)
+    check_fields("three_species", gpu.fields, lambda n: getattr(orc.fields, n),
+                 TOL_1STEP[np.dtype(np.float32)], spread=spread)
+    assert gpu.last_residual <= TOL_RESID[np.dtype(np.float32)]
+
+
+def test_multi_gpu_plumbing_on_one_device():
+    """kwb_enable_peer_access to the own device is a no-op success and
+    kwb_copy_async copies on the caller's stream (the z-slab plane pulls)."""
+    from paper_1606_02862_b200 import _lib
+    _lib.load()
+    _lib.call("kwb_enable_peer_access", torch.cuda.current_device())
+    a = torch.arange(4096, dtype=torch.float32, device="cuda")
+    b = torch.zeros_like(a)
+    _lib.call("kwb_copy_async", b.data_ptr(), a.data_ptr(), a.numel() * 4,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
