@@ -184,6 +184,17 @@ int kwb_particles_advance_species(const kwb_grid *g, int32_t n_species, const kw
                                   int32_t *status, kwb_stream_t stream);
 int kwb_particles_shift_species(const kwb_grid *g, int32_t n_species, const kwb_store *out,
                                 const kwb_exchange *ex, int32_t *status, kwb_stream_t stream);
+/* The same particle phase with each species' advance split in two kernels:
+ * a dense gather/push/move pass writing new offsets, momenta and cell
+ * carries into the workspace store ws[i] (same frames_per_sc as in[i]; its
+ * front/back are ignored), then the deposit + in-super-cell shift pass that
+ * reads them.  Identical results to kwb_particles_advance_species; PCS
+ * (shape_order 3) or ws == NULL falls through to it. */
+int kwb_particles_advance_split(const kwb_grid *g, int32_t n_species, const kwb_species *sp,
+                                const kwb_store *in, const kwb_store *out, const kwb_store *ws,
+                                const kwb_exchange *ex, void *const E[3], void *const B[3],
+                                void *const J[3], void *const *j_planes, int shape_order,
+                                int32_t *status, kwb_stream_t stream);
 
 /* Multi-GPU plumbing for the fused z-slab halo (pic/decomp.py): enable
  * access from the CURRENT device to peer_device (already enabled = OK), and

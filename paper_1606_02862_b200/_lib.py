@@ -71,6 +71,8 @@ _SIGS = {
     "kwb_particles_shift": ([P, P, P, P, P], ctypes.c_int),
     "kwb_particles_advance_species": ([P, ctypes.c_int32, P, P, P, P, Ptr3, Ptr3, Ptr3, P,
                                        ctypes.c_int, P, P], ctypes.c_int),
+    "kwb_particles_advance_split": ([P, ctypes.c_int32, P, P, P, P, P, Ptr3, Ptr3, Ptr3, P,
+                                     ctypes.c_int, P, P], ctypes.c_int),
     "kwb_particles_shift_species": ([P, ctypes.c_int32, P, P, P, P], ctypes.c_int),
     "kwb_fields_faraday_half": ([P, Ptr3, Ptr3, D, P], ctypes.c_int),
     "kwb_fields_ampere": ([P, Ptr3, Ptr3, Ptr3, D, P], ctypes.c_int),

@@ -189,14 +189,19 @@ struct AdvLayout {
     size_t off_jt, off_qf, off_qi, off_arr, off_pf, off_wrap, off_wb, off_ws, bytes;
 };
 
-template <typename F, int ORDER, int NS = 1>
+// per-particle values prefetched into shared memory: the 7 input arrays, or
+// (split path) 3 old offsets, 3 new offsets, 3 new momenta, weight, carries
+template <bool SPLIT>
+constexpr int kPf = SPLIT ? 11 : 7;
+
+template <typename F, int ORDER, int NS = 1, bool SPLIT = false>
 __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     constexpr int H = Shape<ORDER>::H;
     AdvLayout L;
     L.tx = scx + 2; L.ty = scy + 2; L.tz = scz + 2; L.TV = L.tx * L.ty * L.tz;
     L.jx = scx + 2 * H; L.jy = scy + 2 * H; L.jz = scz + 2 * H; L.JV = L.jx * L.jy * L.jz;
     using C = AdvCfg<F, ORDER>;
-    size_t o = (size_t)6 * L.TV * sizeof(typename C::EB);
+    size_t o = SPLIT ? 0 : (size_t)6 * L.TV * sizeof(typename C::EB);   // split: no E/B tile
     o = (o + 127) & ~size_t(127);   // TMA source/destination: 128-byte aligned
     L.off_jt = o;
     o += (size_t)3 * L.JV * sizeof(F);
@@ -208,7 +213,7 @@ __host__ __device__ inline AdvLayout adv_layout(int scx, int scy, int scz) {
     L.off_arr = o;
     o += (size_t)NS * kMaxCells * sizeof(int);   // in-super-cell arrivals per species
     L.off_pf = o;
-    o += (size_t)2 * 7 * kMaxCells * sizeof(F);   // double-buffered next-particle records
+    o += (size_t)2 * kPf<SPLIT> * kMaxCells * sizeof(F);   // double-buffered next-particle records
     L.off_wrap = o;
     o += (size_t)(L.tx + L.ty + L.tz + L.jx + L.jy + L.jz) * sizeof(int);
     o = (o + 15) & ~size_t(15);
@@ -268,6 +273,84 @@ __device__ __forceinline__ double sample_sel(const TT *__restrict__ T, const AxF
     const double c01 = a01 * gx + b01 * fx;
     const double c11 = a11 * gx + b11 * fx;
     return (c00 * (1.0 - fy) + c10 * fy) * (1.0 - fz) + (c01 * (1.0 - fy) + c11 * fy) * fz;
+}
+
+// The six gathered components of one particle from the staged float64 tile
+// (pic/kernels.py:53-77): floor-free trilinear samples, rounded to F.
+template <typename F, typename EB>
+__device__ __forceinline__ void gather6(const EB *__restrict__ ebd, int TV, int tx, int txy,
+                                        int tbase, double px, double py, double pz, double cxd,
+                                        double cyd, double czd, F &e0, F &e1, F &e2, F &b0, F &b1,
+                                        F &b2) {
+    const AxFrac ax[3][2] = {{ax_frac(px, 0.5, cxd, cxd - 1.0), ax_frac(px, 1.0, cxd, cxd - 1.0)},
+                             {ax_frac(py, 0.5, cyd, cyd - 1.0), ax_frac(py, 1.0, cyd, cyd - 1.0)},
+                             {ax_frac(pz, 0.5, czd, czd - 1.0), ax_frac(pz, 1.0, czd, czd - 1.0)}};
+    e0 = (F)sample_sel<0>(ebd, ax, tbase, tx, txy, TV);
+    e1 = (F)sample_sel<1>(ebd + TV, ax, tbase, tx, txy, TV);
+    e2 = (F)sample_sel<2>(ebd + 2 * TV, ax, tbase, tx, txy, TV);
+    b0 = (F)sample_sel<3>(ebd + 3 * TV, ax, tbase, tx, txy, TV);
+    b1 = (F)sample_sel<4>(ebd + 4 * TV, ax, tbase, tx, txy, TV);
+    b2 = (F)sample_sel<5>(ebd + 5 * TV, ax, tbase, tx, txy, TV);
+}
+
+// Carries of the move packed for the split path's deposit kernel (4 bits
+// each, biased by 8; a carry outside -8..7 is clamped -- any |carry| > 1 is
+// a ContractViolation there).
+__device__ __forceinline__ int pack_carries(int dx, int dy, int dz) {
+    dx = min(max(dx, -8), 7);
+    dy = min(max(dy, -8), 7);
+    dz = min(max(dz, -8), 7);
+    return (dx + 8) | ((dy + 8) << 4) | ((dz + 8) << 8);
+}
+__device__ __forceinline__ void unpack_carries(int code, int &dx, int &dy, int &dz) {
+    dx = (code & 15) - 8;
+    dy = ((code >> 4) & 15) - 8;
+    dz = ((code >> 8) & 15) - 8;
+}
+
+// Boris push (pic/kernels.py:80-104) and move (:107-135) of one particle,
+// bit for bit the reference: float64 without contraction, the three
+// quotients by one divisor through one reciprocal (div_rcp), gamma of the
+// move from storage-type squares, offsets rounded to F (1.0 kept).  Returns
+// the new momentum, the new offsets and the floor carries of the move.
+template <typename F>
+__device__ __forceinline__ void push_move(double qm, const double (&dt_d)[3], F e0, F e1, F e2,
+                                          F b0, F b1, F b2, F ox, F oy, F oz, F ux, F uy, F uz,
+                                          F &nux, F &nuy, F &nuz, F &nox, F &noy, F &noz,
+                                          int &dxi, int &dyi, int &dzi) {
+    const double qe0 = qm * (double)e0, qe1 = qm * (double)e1, qe2 = qm * (double)e2;
+    const double umx = (double)ux + qe0;
+    const double umy = (double)uy + qe1;
+    const double umz = (double)uz + qe2;
+    const double gm = sqrt(((1.0 + umx * umx) + umy * umy) + umz * umz);
+    const double rgm = 1.0 / gm;
+    const double ttx = div_rcp(qm * (double)b0, gm, rgm);
+    const double tty = div_rcp(qm * (double)b1, gm, rgm);
+    const double ttz = div_rcp(qm * (double)b2, gm, rgm);
+    const double tsq1 = 1.0 + ((ttx * ttx + tty * tty) + ttz * ttz);
+    const double rts = 1.0 / tsq1;
+    const double ssx = div_rcp(2.0 * ttx, tsq1, rts);
+    const double ssy = div_rcp(2.0 * tty, tsq1, rts);
+    const double ssz = div_rcp(2.0 * ttz, tsq1, rts);
+    const double upx = umx + (umy * ttz - umz * tty);
+    const double upy = umy + (umz * ttx - umx * ttz);
+    const double upz = umz + (umx * tty - umy * ttx);
+    nux = (F)((umx + (upy * ssz - upz * ssy)) + qe0);
+    nuy = (F)((umy + (upz * ssx - upx * ssz)) + qe1);
+    nuz = (F)((umz + (upx * ssy - upy * ssx)) + qe2);
+    // move: gamma from F squares
+    const F sxx = nux * nux, syy = nuy * nuy, szz = nuz * nuz;
+    const double gv = sqrt(((1.0 + (double)sxx) + (double)syy) + (double)szz);
+    const double rgv = 1.0 / gv;
+    const double mpx = (double)ox + div_rcp((double)nux, gv, rgv) * dt_d[0];
+    const double mpy = (double)oy + div_rcp((double)nuy, gv, rgv) * dt_d[1];
+    const double mpz = (double)oz + div_rcp((double)nuz, gv, rgv) * dt_d[2];
+    dxi = (int)floor(mpx);
+    dyi = (int)floor(mpy);
+    dzi = (int)floor(mpz);
+    nox = (F)(mpx - (double)dxi);
+    noy = (F)(mpy - (double)dyi);
+    noz = (F)(mpz - (double)dzi);
 }
 
 template <int C, typename TT>
@@ -1022,12 +1105,17 @@ __device__ __forceinline__ void fill_tab(SpTab<F> &T, const StoreT<F> &in, const
 }
 
 // SX/SY/SZ: compile-time super cell (0 = runtime, from g).
-template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS>
+// SPLIT (NS = 1 only): the gather/push/move already ran in push_kernel
+// (csrc/push.cuh), whose workspace store arrives as sb.in; this kernel only
+// deposits and shifts.
+template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS, bool SPLIT = false>
 __global__ void __launch_bounds__(kMaxCells, AdvCfg<F, ORDER>::kMinBlocks)
 advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, FieldPtrs fp,
                int32_t *__restrict__ status, const __grid_constant__ CUtensorMap tm_eb, int tma,
                SpeciesB<F> sb, int sp0) {
     static_assert(NS == 1 || NS == 2, "one or two species per launch");
+    static_assert(!SPLIT || NS == 1, "the split path advances one species per launch");
+    constexpr int NPF = kPf<SPLIT>;
     constexpr int H = Shape<ORDER>::H;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ int s_maxcol, s_maxcol1;
@@ -1035,7 +1123,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
 
     const int scx = SX ? SX : g.scx, scy = SY ? SY : g.scy, scz = SZ ? SZ : g.scz;
     const int V = scx * scy * scz;
-    const AdvLayout L = adv_layout<F, ORDER, NS>(scx, scy, scz);
+    const AdvLayout L = adv_layout<F, ORDER, NS, SPLIT>(scx, scy, scz);
     const int K = in.frames;
     __shared__ SpTab<F> tab[NS];
     if (NS == 2) {
@@ -1094,8 +1182,21 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     auto prefetch = [&](int i) {
         if (i < n_t) {
             const int64_t q = slot_of(i);
-            F *d = pf + (i & 1) * 7 * kMaxCells;
-            if (NS == 2) {
+            F *d = pf + (i & 1) * NPF * kMaxCells;
+            if (SPLIT) {
+                const StoreT<F> &ws = sb.in;
+                cp_async_elem(d + 0 * kMaxCells, in.ox + q);
+                cp_async_elem(d + 1 * kMaxCells, in.oy + q);
+                cp_async_elem(d + 2 * kMaxCells, in.oz + q);
+                cp_async_elem(d + 3 * kMaxCells, ws.ox + q);
+                cp_async_elem(d + 4 * kMaxCells, ws.oy + q);
+                cp_async_elem(d + 5 * kMaxCells, ws.oz + q);
+                cp_async_elem(d + 6 * kMaxCells, ws.ux + q);
+                cp_async_elem(d + 7 * kMaxCells, ws.uy + q);
+                cp_async_elem(d + 8 * kMaxCells, ws.uz + q);
+                cp_async_elem(d + 9 * kMaxCells, in.w + q);
+                cp_async_elem(d + 10 * kMaxCells, ws.w + q);
+            } else if (NS == 2) {
                 const SpTab<F> &T = tab[species_of(i)];
 #pragma unroll
                 for (int a = 0; a < 7; ++a) cp_async_elem(d + a * kMaxCells, T.in[a] + q);
@@ -1124,7 +1225,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     // at origin - 4 (f32) / origin - 2 (f64) instead of origin - 1.
     const bool interior = bx >= 1 && bx + 2 <= g.gx && by >= 1 && by + 2 <= g.gy && bz >= 1 &&
                           bz + 2 <= g.gz;
-    const bool tma_eb = REGACC && (tma & TMA_EB) && interior;
+    const bool tma_eb = !SPLIT && REGACC && (tma & TMA_EB) && interior;
     constexpr int kTmaX0 = sizeof(F) == 4 ? 4 : 2;        // box x start = origin - kTmaX0
     const int boxx = (L.tx + kTmaX0 - 1 + (16 / (int)sizeof(F)) - 1) / (16 / (int)sizeof(F)) *
                      (16 / (int)sizeof(F));                // covers origin - 1 .. origin + scx
@@ -1164,7 +1265,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             const int b = r2 / L.tx, a = r2 - b * L.tx;
             ebd[i] = (EB)src[((c * L.tz + d) * L.ty + b) * boxx + a + kTmaX0 - 1];
         }
-    } else {
+    } else if (!SPLIT) {
         // flat over (component, z, y, x) so every lane works, and batches of
         // kStageB independent loads in flight per thread (one memory latency
         // per batch instead of one per tile row)
@@ -1297,23 +1398,30 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
         const bool active = i < n_t;
         const int sp_i = species_of(i);   // this particle's species (0 unless NS = 2)
         cp_async_wait_all();
-        const F *cur = pf + (i & 1) * 7 * kMaxCells;
+        const F *cur = pf + (i & 1) * NPF * kMaxCells;
         prefetch(i + 1);
         // read at their uses, not hoisted into registers (measured: hoisting
         // all seven costs 5 %)
         const F &ox = cur[0 * kMaxCells], &oy = cur[1 * kMaxCells], &oz = cur[2 * kMaxCells],
                 &ux = cur[3 * kMaxCells], &uy = cur[4 * kMaxCells], &uz = cur[5 * kMaxCells],
-                &w = cur[6 * kMaxCells];
+                &w = cur[(SPLIT ? 9 : 6) * kMaxCells];
         bool queue = false, leave = false, mover = false, stay = false, pstay = false;
         F nox = 0, noy = 0, noz = 0, nux = 0, nuy = 0, nuz = 0;
         int dcx = 0, dcy = 0, dcz = 0, ncx = 0, ncy = 0, ncz = 0, dest = 0, nlc = 0;
         if (active) {
-            // -- gather (pic/kernels.py:53-77): f64 compute, F store --------
-            const double px = cxd + (double)ox, py = cyd + (double)oy, pz = czd + (double)oz;
 #ifdef KWB_EARLY_S0
             float s0w[3][3];
             if constexpr (REGACC && sizeof(F) == 4) old_weights<ORDER>((float)ox, (float)oy, (float)oz, s0w);
 #endif
+            int dxi, dyi, dzi;
+            if constexpr (SPLIT) {
+                // push_kernel's results (csrc/push.cuh)
+                nox = cur[3 * kMaxCells]; noy = cur[4 * kMaxCells]; noz = cur[5 * kMaxCells];
+                nux = cur[6 * kMaxCells]; nuy = cur[7 * kMaxCells]; nuz = cur[8 * kMaxCells];
+                unpack_carries((int)cur[10 * kMaxCells], dxi, dyi, dzi);
+            } else {
+            // -- gather (pic/kernels.py:53-77): f64 compute, F store --------
+            const double px = cxd + (double)ox, py = cyd + (double)oy, pz = czd + (double)oz;
             const int ox0 = orgx - 1, oy0 = orgy - 1, oz0 = orgz - 1;
 #if defined(KWB_GATHER_FLOOR)
             const F e0 = (F)sample_tile<0>(EBx, px, py, pz, ox0, oy0, oz0, L.tx, txy);
@@ -1338,40 +1446,12 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
             const F b0 = e0, b1 = e1, b2 = e2;
 #endif
 
-            // -- Boris push (pic/kernels.py:80-104), all in double ---------
+            // -- Boris push + move (pic/kernels.py:80-135), shared with the
+            // split path's push_kernel (csrc/push.cuh)
             const double qm = NS == 2 ? tab[sp_i].qm : qm0;
-            const double qe0 = qm * (double)e0, qe1 = qm * (double)e1, qe2 = qm * (double)e2;
-            const double umx = (double)ux + qe0;
-            const double umy = (double)uy + qe1;
-            const double umz = (double)uz + qe2;
-            const double gm = sqrt(((1.0 + umx * umx) + umy * umy) + umz * umz);
-            const double rgm = 1.0 / gm;
-            const double ttx = div_rcp(qm * (double)b0, gm, rgm);
-            const double tty = div_rcp(qm * (double)b1, gm, rgm);
-            const double ttz = div_rcp(qm * (double)b2, gm, rgm);
-            const double tsq1 = 1.0 + ((ttx * ttx + tty * tty) + ttz * ttz);
-            const double rts = 1.0 / tsq1;
-            const double ssx = div_rcp(2.0 * ttx, tsq1, rts);
-            const double ssy = div_rcp(2.0 * tty, tsq1, rts);
-            const double ssz = div_rcp(2.0 * ttz, tsq1, rts);
-            const double upx = umx + (umy * ttz - umz * tty);
-            const double upy = umy + (umz * ttx - umx * ttz);
-            const double upz = umz + (umx * tty - umy * ttx);
-            nux = (F)((umx + (upy * ssz - upz * ssy)) + qe0);
-            nuy = (F)((umy + (upz * ssx - upx * ssz)) + qe1);
-            nuz = (F)((umz + (upx * ssy - upy * ssx)) + qe2);
-
-            // -- move (pic/kernels.py:107-135): gamma from F squares -------
-            const F sxx = nux * nux, syy = nuy * nuy, szz = nuz * nuz;
-            const double gv = sqrt(((1.0 + (double)sxx) + (double)syy) + (double)szz);
-            const double rgv = 1.0 / gv;
-            const double mpx = (double)ox + div_rcp((double)nux, gv, rgv) * sp.dt_d[0];
-            const double mpy = (double)oy + div_rcp((double)nuy, gv, rgv) * sp.dt_d[1];
-            const double mpz = (double)oz + div_rcp((double)nuz, gv, rgv) * sp.dt_d[2];
-            const int dxi = (int)floor(mpx), dyi = (int)floor(mpy), dzi = (int)floor(mpz);
-            nox = (F)(mpx - (double)dxi);
-            noy = (F)(mpy - (double)dyi);
-            noz = (F)(mpz - (double)dzi);
+            push_move<F>(qm, sp.dt_d, e0, e1, e2, b0, b1, b2, ox, oy, oz, ux, uy, uz, nux, nuy, nuz,
+                         nox, noy, noz, dxi, dyi, dzi);
+            }
 
             // -- cell, membership (pic/particles.py:226-228), deposit route
             const int nlx = lx + dxi, nly = ly + dyi, nlz = lz + dzi;

@@ -33,6 +33,7 @@
 namespace kwb {
 
 #include "advance.cuh"
+#include "push.cuh"
 
 // Append leavers to the back of their new column (the cross-super-cell
 // shift, pic/particles.py:316-345).  Slot claims are atomic per column.
@@ -495,15 +496,18 @@ static int shift_all(const kwb_grid *g, int n, const kwb_store *out, const kwb_e
 }
 
 // sp / in / out: NS entries; status: NS x KWB_STATUS_WORDS
-template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS>
+// SPLIT: push_kernel (gather/push/move into the workspace store ws) then
+// the deposit/shift kernel reading it (csrc/push.cuh).
+template <typename F, int ORDER, bool REGACC, int SX, int SY, int SZ, int NS, bool SPLIT = false>
 static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
                           const kwb_store *out, const kwb_exchange *ex, void *const E[3],
                           void *const B[3], void *const J[3], void *const *jpl,
-                          int32_t *status, cudaStream_t stream, int sp0, bool reset) {
+                          int32_t *status, cudaStream_t stream, int sp0, bool reset,
+                          const kwb_store *ws = nullptr) {
     Geo geo = geo_of(*g);
     const int threads = block_threads(g);
-    const size_t smem = adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).bytes;
-    auto kern = advance_kernel<F, ORDER, REGACC, SX, SY, SZ, NS>;
+    const size_t smem = adv_layout<F, ORDER, NS, SPLIT>(g->scx, g->scy, g->scz).bytes;
+    auto kern = advance_kernel<F, ORDER, REGACC, SX, SY, SZ, NS, SPLIT>;
     if (smem > 227 * 1024) {
         kwb_set_error("super cell too large for the shared-memory tiles (%zu B)", smem);
         return KWB_EINVAL;
@@ -521,6 +525,11 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
     CUtensorMap tm_eb;
     memset(&tm_eb, 0, sizeof(tm_eb));
     int tma = 0;
+    const size_t stage_room =
+        SPLIT ? (size_t)6 * push_layout<F>(g->scx, g->scy, g->scz).boxx * (g->scy + 2) *
+                    (g->scz + 2) * sizeof(F)
+              : adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).off_arr -
+                    adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).off_qf;
     if (REGACC) {
         const cuuint32_t vec = 16 / sizeof(F), x0 = sizeof(F) == 4 ? 4 : 2;
         const cuuint32_t need = (cuuint32_t)g->scx + 1 + x0;   // origin - x0 .. origin + scx
@@ -529,9 +538,7 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
         void *eb[6] = {E[0], E[1], E[2], B[0], B[1], B[2]};
         // the box start origin - x0 is 16-byte aligned when scx is a multiple of x0
         if (g->scx % x0 == 0 && ebox[0] <= 256 && ebox[1] <= 256 && ebox[2] <= 256 &&
-            (size_t)6 * ebox[0] * ebox[1] * ebox[2] * sizeof(F) <=
-                adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).off_arr -
-                    adv_layout<F, ORDER, NS>(g->scx, g->scy, g->scz).off_qf &&
+            (size_t)6 * ebox[0] * ebox[1] * ebox[2] * sizeof(F) <= stage_room &&
             lattice_map<F>(&tm_eb, eb, 6, g, ebox))
             tma |= TMA_EB;
         if (const char *m = getenv("KWB_TMA_MASK")) tma &= atoi(m);   // debugging / A/B
@@ -543,6 +550,17 @@ static int launch_advance(const kwb_grid *g, const kwb_species *sp, const kwb_st
         sb.out = store_of<F>(out[1]);
         sb.sp = sp[1];
         sb.status = status + KWB_STATUS_WORDS;
+    }
+    if constexpr (SPLIT) {
+        const StoreT<F> wst = store_of<F>(ws[0]);
+        auto pk = push_kernel<F, SX, SY, SZ>;
+        const size_t psm = push_layout<F>(g->scx, g->scy, g->scz).bytes;
+        if (psm > 48 * 1024)
+            cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        pk<<<n_sc, threads, psm, stream>>>(geo, sp[0], store_of<F>(in[0]), wst, fp, tm_eb, tma);
+        if (int rc = kwb_check_launch("push_kernel")) return rc;
+        sb.in = wst;
+        tma = 0;
     }
     kern<<<n_sc, threads, smem, stream>>>(geo, sp[0], store_of<F>(in[0]), store_of<F>(out[0]),
                                           exch_of<F>(*ex), fp, status, tm_eb, tma, sb, sp0);
@@ -658,6 +676,71 @@ extern "C" int kwb_particles_advance_species(const kwb_grid *g, int32_t n_specie
     for (int i = 0; i < n_species; ++i) {
         rc = advance_ns<1>(g, sp + i, in + i, out + i, ex, E, B, J, j_planes, shape_order,
                            status + i * KWB_STATUS_WORDS, (cudaStream_t)stream, i, i == 0);
+        if (rc) return rc;
+    }
+    return KWB_OK;
+}
+
+template <typename F, int ORDER>
+static int split_one(const kwb_grid *g, const kwb_species *sp, const kwb_store *in,
+                     const kwb_store *out, const kwb_store *ws, const kwb_exchange *ex,
+                     void *const E[3], void *const B[3], void *const J[3], void *const *jpl,
+                     int32_t *status, cudaStream_t s, int sp0, bool reset) {
+    if (g->scx == 8 && g->scy == 8 && g->scz == 4)
+        return launch_advance<F, ORDER, true, 8, 8, 4, 1, true>(g, sp, in, out, ex, E, B, J, jpl,
+                                                               status, s, sp0, reset, ws);
+    return launch_advance<F, ORDER, true, 0, 0, 0, 1, true>(g, sp, in, out, ex, E, B, J, jpl,
+                                                           status, s, sp0, reset, ws);
+}
+
+// kwb_particles_advance_species with the advance split in two kernels per
+// species (csrc/push.cuh): ws[i] is a workspace store of in[i]'s geometry
+// (same frames_per_sc; its front/back are not used).  PCS keeps the fused
+// kernel (ws ignored).
+extern "C" int kwb_particles_advance_split(const kwb_grid *g, int32_t n_species,
+                                           const kwb_species *sp, const kwb_store *in,
+                                           const kwb_store *out, const kwb_store *ws,
+                                           const kwb_exchange *ex, void *const E[3],
+                                           void *const B[3], void *const J[3],
+                                           void *const *j_planes, int shape_order,
+                                           int32_t *status, kwb_stream_t stream) {
+    if (shape_order == 3 || !ws)
+        return kwb_particles_advance_species(g, n_species, sp, in, out, ex, E, B, J, j_planes,
+                                             shape_order, status, stream);
+    int rc = check_grid(g);
+    if (rc) return rc;
+    if (n_species < 1 || n_species > kMaxSpecies || !sp || !in || !out || !ex || !ex->count ||
+        !status || !E || !B || !J) {
+        kwb_set_error("advance_split: NULL argument or bad species count");
+        return KWB_EINVAL;
+    }
+    if (shape_order != 1 && shape_order != 2) {
+        kwb_set_error("shape_order must be 1 (CIC), 2 (TSC) or 3 (PCS), got %d", shape_order);
+        return KWB_EINVAL;
+    }
+    for (int i = 0; i < n_species; ++i) {
+        if ((rc = check_store(in + i, "input")) || (rc = check_store(out + i, "output")) ||
+            (rc = check_store(ws + i, "workspace")))
+            return rc;
+        if (out[i].frames_per_sc != in[i].frames_per_sc ||
+            ws[i].frames_per_sc != in[i].frames_per_sc) {
+            kwb_set_error("advance_split: input, output and workspace differ in frames_per_sc");
+            return KWB_EINVAL;
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int i = 0; i < n_species; ++i) {
+        int32_t *st = status + i * KWB_STATUS_WORDS;
+        const bool f32 = g->dtype == KWB_F32;
+        rc = shape_order == 1
+                 ? (f32 ? split_one<float, 1>(g, sp + i, in + i, out + i, ws + i, ex, E, B, J,
+                                              j_planes, st, s, i, i == 0)
+                        : split_one<double, 1>(g, sp + i, in + i, out + i, ws + i, ex, E, B, J,
+                                               j_planes, st, s, i, i == 0))
+                 : (f32 ? split_one<float, 2>(g, sp + i, in + i, out + i, ws + i, ex, E, B, J,
+                                              j_planes, st, s, i, i == 0)
+                        : split_one<double, 2>(g, sp + i, in + i, out + i, ws + i, ex, E, B, J,
+                                               j_planes, st, s, i, i == 0));
         if (rc) return rc;
     }
     return KWB_OK;

@@ -129,6 +129,14 @@ class SuperCellStore:
     def swap(self) -> None:
         self._cols.reverse()
 
+    def workspace(self) -> _Columns:
+        """Scratch columns of the split advance (kwb_particles_advance_split:
+        new offsets, momenta and carries per slot), sized like the store."""
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.frames != self.frames_per_sc:
+            self._ws = ws = self._new_columns()
+        return ws
+
     def reserve(self, max_column: int, stream=None) -> bool:
         """Grow frames_per_sc so the fullest column sits below GROW_AT of it;
         repacks the live particles on the device.  Returns True if it grew."""

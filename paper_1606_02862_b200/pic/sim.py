@@ -154,6 +154,10 @@ class Simulation:
         # one particle-phase call for all species (two species: one fused
         # launch); False: the reference's per-species launches
         self.fuse_species = os.environ.get("KWB_PER_SPECIES", "0") != "1" and len(p.species) <= 4
+        # advance as two kernels per species (dense push, then deposit/shift;
+        # csrc/push.cuh) -- CIC/TSC only
+        self.split_advance = (self.fuse_species and self.shape_order != 3 and
+                              os.environ.get("KWB_SPLIT", "0") == "1")
         self._status = torch.zeros((len(p.species), _lib.STATUS_WORDS), dtype=torch.int32,
                                    device=self.device)
         self._status_host = torch.zeros_like(self._status, device="cpu").pin_memory()
@@ -255,6 +259,8 @@ class Simulation:
         for st in self.stores:
             st.spare()   # both column buffers exist before a capture
             key += [st._cols[0].ox.data_ptr(), st._cols[1].ox.data_ptr(), st.frames_per_sc]
+            if self.split_advance:
+                key.append(st.workspace().ox.data_ptr())
         return tuple(key)
 
     def _graph_step(self):
@@ -324,10 +330,17 @@ class Simulation:
             outs = (_lib.StoreC * n)(*[st.spare().cstruct() for st in self.stores])
             sps = (_lib.SpeciesC * n)(*self._species)
             with _nvtx("advance[all species]"):
-                _lib.call("kwb_particles_advance_species", g, n, sps, ins, outs,
-                          ctypes.byref(ex.cstruct), E, B, J,
-                          jpl.data_ptr() if jpl is not None else None,
-                          self.shape_order, self._status.data_ptr(), stream)
+                if self.split_advance:
+                    wss = (_lib.StoreC * n)(*[st.workspace().cstruct() for st in self.stores])
+                    _lib.call("kwb_particles_advance_split", g, n, sps, ins, outs, wss,
+                              ctypes.byref(ex.cstruct), E, B, J,
+                              jpl.data_ptr() if jpl is not None else None,
+                              self.shape_order, self._status.data_ptr(), stream)
+                else:
+                    _lib.call("kwb_particles_advance_species", g, n, sps, ins, outs,
+                              ctypes.byref(ex.cstruct), E, B, J,
+                              jpl.data_ptr() if jpl is not None else None,
+                              self.shape_order, self._status.data_ptr(), stream)
             with _nvtx("shift[all species]"):
                 _lib.call("kwb_particles_shift_species", g, n, outs, ctypes.byref(ex.cstruct),
                           self._status.data_ptr(), stream)

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("libs", nargs="+", help="library paths; LIB@VAR=VAL sets an env var for that arm")
     a = ap.parse_args()
     res = {lib: [] for lib in a.libs}
@@ -31,7 +32,7 @@ def main():
                 k, _, v = kv.partition("=")
                 env[k] = v
             out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", a.config,
-                                  "--steps", str(a.steps), "--warmup", "3", "--no-cpu"],
+                                  "--steps", str(a.steps), "--warmup", str(a.warmup), "--no-cpu"],
                                  capture_output=True, text=True, env=env, cwd=ROOT)
             try:
                 d = json.loads(out.stdout.strip().splitlines()[-1])
