@@ -76,8 +76,14 @@ class YeeFieldSet:
 
     def load_numpy(self, name: str, arr) -> None:
         """Upload a reference-ordered (nx, ny, nz) host array into one lattice."""
-        a = torch.as_tensor(np.asarray(arr, dtype=self.dtype))
-        self._storage[name].copy_(a.permute(2, 1, 0).to(self.device))
+        if isinstance(arr, torch.Tensor):
+            a = arr.to(TORCH_DTYPE[self.dtype])   # no copy if the dtype matches
+        else:
+            a = torch.as_tensor(np.ascontiguousarray(arr, dtype=self.dtype))
+        # copy as laid out (pinned host memory: asynchronous DMA), transpose
+        # to x-fastest on the device
+        d = a.to(self.device, non_blocking=True)
+        self._storage[name].copy_(d.permute(2, 1, 0))
 
     def zero_current(self) -> None:
         """J = 0 on the current stream (kwb_zero_step)."""

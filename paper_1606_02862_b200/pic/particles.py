@@ -344,19 +344,29 @@ class SuperCellStore:
                   n, d_cells[0].data_ptr(), d_cells[1].data_ptr(), d_cells[2].data_ptr(),
                   _lib.ptr7(d_f), status.data_ptr(), _stream(stream, self.device))
 
-    def load_packed(self, arrays: dict, stream=None, presorted: bool = False) -> None:
-        """Replace the store's content with particle records (global cells
-        cx/cy/cz plus ox oy oz ux uy uz w; host numpy or device tensors).
-        Columns are sized from the fullest cell with headroom; the load
-        kernel appends every record to its column."""
-        del presorted  # any order is accepted
-
+    def upload(self, arrays: dict) -> dict:
+        """The records of `arrays` as device tensors of the store's types
+        (asynchronous from pinned host memory)."""
         def up(a, tdt):
             t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))
             return t.to(device=self.device, dtype=tdt, non_blocking=True).contiguous()
+        d = {c: up(arrays[c], torch.int32) for c in ("cx", "cy", "cz")}
+        d.update({c: up(arrays[c], self.tdtype) for c in FLOAT_COLUMNS})
+        return d
 
-        d_cells = [up(arrays[c], torch.int32) for c in ("cx", "cy", "cz")]
-        d_f = [up(arrays[c], self.tdtype) for c in FLOAT_COLUMNS]
+    def load_packed(self, arrays: dict, stream=None, presorted: bool = False,
+                    deferred: bool = False):
+        """Replace the store's content with particle records (global cells
+        cx/cy/cz plus ox oy oz ux uy uz w; host numpy or device tensors).
+        Columns are sized from the fullest cell with headroom; the load
+        kernel appends every record to its column.  deferred=True: return
+        the device status words instead of checking them (the caller checks
+        several stores with one synchronisation and reloads a failed one
+        with deferred=False)."""
+        del presorted  # any order is accepted
+        d = self.upload(arrays)
+        d_cells = [d[c] for c in ("cx", "cy", "cz")]
+        d_f = [d[c] for c in FLOAT_COLUMNS]
         n = d_cells[0].shape[0]
         nx, ny, nz = self.cells.as_tuple()
         if n:
@@ -378,6 +388,8 @@ class SuperCellStore:
                       _lib.ctypes.byref(self.current.cstruct()), n, d_cells[0].data_ptr(),
                       d_cells[1].data_ptr(), d_cells[2].data_ptr(), _lib.ptr7(d_f),
                       status.data_ptr(), _stream(stream, self.device))
+            if deferred:
+                return status
             bad = int(status[_lib.ST_LOAD_ERRORS].item())
             if not bad:
                 return

@@ -422,8 +422,16 @@ class Simulation:
         if particles is not None:
             if len(particles) != len(self.stores):
                 raise ValueError("one particle dict per species expected")
-            for st, arrays in zip(self.stores, particles):
-                st.load_packed(arrays)
+            # every species' records on their way before the first load
+            # kernel, one synchronisation for all the load checks
+            dev = [st.upload(arrays) for st, arrays in zip(self.stores, particles)]
+            status = [st.load_packed(d, deferred=True) for st, d in zip(self.stores, dev)]
+            bad = torch.stack([s_[_lib.ST_LOAD_ERRORS] for s_ in status if s_ is not None]) \
+                if any(s_ is not None for s_ in status) else None
+            if bad is not None and int(bad.max()) > 0:
+                for st, d, s_ in zip(self.stores, dev, status):
+                    if s_ is not None and int(s_[_lib.ST_LOAD_ERRORS]) > 0:
+                        st.load_packed(d)   # columns sized from the fullest cell
         self._rho_prev = None
         self._G_prev = None
 
