@@ -1135,6 +1135,31 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     const int sc = blockIdx.x;
     const int bx = sc % g.gx, by = (sc / g.gx) % g.gy, bz = sc / (g.gx * g.gy);
     const int orgx = bx * scx, orgy = by * scy, orgz = bz * scz;
+
+    // TMA for super cells whose E/B guard lies inside the grid (no periodic
+    // wrap; the seams keep the indexed path): one elected thread loads the
+    // 6-lattice E/B box (cp.async.bulk.tensor, completion on an mbarrier)
+    // into the still unused queue area, and the CTA widens it into the
+    // float64 tile.  kwb_particles_advance builds the tensor map when the
+    // lattices are equally spaced (TMA_EB).  The box's x start must be
+    // 16-byte aligned on B200 (measured: an unaligned start raises an
+    // illegal-instruction fault, tools/probe/tma_probe2.cu), so it starts
+    // at origin - 4 (f32) / origin - 2 (f64) instead of origin - 1.  Issued
+    // first thing, so its latency overlaps the column-count loads.
+    const bool interior = bx >= 1 && bx + 2 <= g.gx && by >= 1 && by + 2 <= g.gy && bz >= 1 &&
+                          bz + 2 <= g.gz;
+    const bool tma_eb = !SPLIT && REGACC && (tma & TMA_EB) && interior;
+    constexpr int kTmaX0 = sizeof(F) == 4 ? 4 : 2;        // box x start = origin - kTmaX0
+    const int boxx = (L.tx + kTmaX0 - 1 + (16 / (int)sizeof(F)) - 1) / (16 / (int)sizeof(F)) *
+                     (16 / (int)sizeof(F));                // covers origin - 1 .. origin + scx
+    void *eb_dst = (void *)(smem_raw + L.off_qf);
+    if (tma_eb && t == 0) {
+        mbar_init(&s_mbar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&s_mbar, (unsigned)(6 * boxx * L.ty * L.tz * sizeof(F)));
+        tma_load_4d(eb_dst, &tm_eb, orgx - kTmaX0, orgy - 1, orgz - 1, 0, &s_mbar);
+    }
+
     const int lx = t % scx, ly = (t / scx) % scy, lz = t / (scx * scy);
 
     using EB = typename AdvCfg<F, ORDER>::EB;
@@ -1158,6 +1183,7 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     const int n_t = n0 + front1 + back1;         // the lane's sequence: species 0, then 1
     // empty super cell (e.g. a z-slab guard layer): nothing to stage or deposit
     if (__syncthreads_or(n_t) == 0) {
+        if (tma_eb && t == 0) mbar_wait(&s_mbar, 0);   // no exit with the box in flight
         if (owner) {
             out.front[col] = 0; out.back[col] = 0;
             if (NS == 2) { sb.out.front[col] = 0; sb.out.back[col] = 0; }
@@ -1214,29 +1240,6 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     };
     prefetch(0);   // issued before the staging: its latency overlaps it
 
-    // TMA for super cells whose E/B guard lies inside the grid (no periodic
-    // wrap; the seams keep the indexed path): one elected thread loads the
-    // 6-lattice E/B box (cp.async.bulk.tensor, completion on an mbarrier)
-    // into the still unused queue area, and the CTA widens it into the
-    // float64 tile.  kwb_particles_advance builds the tensor map when the
-    // lattices are equally spaced (TMA_EB).  The box's x start must be
-    // 16-byte aligned on B200 (measured: an unaligned start raises an
-    // illegal-instruction fault, tools/probe/tma_probe2.cu), so it starts
-    // at origin - 4 (f32) / origin - 2 (f64) instead of origin - 1.
-    const bool interior = bx >= 1 && bx + 2 <= g.gx && by >= 1 && by + 2 <= g.gy && bz >= 1 &&
-                          bz + 2 <= g.gz;
-    const bool tma_eb = !SPLIT && REGACC && (tma & TMA_EB) && interior;
-    constexpr int kTmaX0 = sizeof(F) == 4 ? 4 : 2;        // box x start = origin - kTmaX0
-    const int boxx = (L.tx + kTmaX0 - 1 + (16 / (int)sizeof(F)) - 1) / (16 / (int)sizeof(F)) *
-                     (16 / (int)sizeof(F));                // covers origin - 1 .. origin + scx
-    void *eb_dst = (void *)(smem_raw + L.off_qf);
-    if (tma_eb && t == 0) {
-        mbar_init(&s_mbar, 1);
-        fence_mbar_init();
-        mbar_expect_tx(&s_mbar, (unsigned)(6 * boxx * L.ty * L.tz * sizeof(F)));
-        tma_load_4d(eb_dst, &tm_eb, orgx - kTmaX0, orgy - 1, orgz - 1, 0, &s_mbar);
-    }
-
     // ---- periodic index tables, then stage E/B and clear the J tile -------
     for (int i = t; i < L.tx; i += blockDim.x) wtx[i] = pymod(orgx - 1 + i, g.nx);
     for (int i = t; i < L.ty; i += blockDim.x) wty[i] = pymod(orgy - 1 + i, g.ny);
@@ -1257,13 +1260,13 @@ advance_kernel(Geo g, kwb_species sp, StoreT<F> in, StoreT<F> out, ExchT<F> ex, 
     if (tma_eb) {
         mbar_wait(&s_mbar, 0);
         // widen / copy the box (x from origin - kTmaX0) into the tile (x from origin - 1)
-        const F *src = reinterpret_cast<const F *>(eb_dst);
-        const int total = 6 * L.TV, txy_ = L.tx * L.ty;
+        // element i = row * tx + a of the tile, row = (c * tz + d) * ty + b,
+        // is element row * boxx + a + kTmaX0 - 1 of the box
+        const F *src = reinterpret_cast<const F *>(eb_dst) + kTmaX0 - 1;
+        const int total = 6 * L.TV;
         for (int i = t; i < total; i += blockDim.x) {
-            const int c = i / L.TV, r = i - c * L.TV;
-            const int d = r / txy_, r2 = r - d * txy_;
-            const int b = r2 / L.tx, a = r2 - b * L.tx;
-            ebd[i] = (EB)src[((c * L.tz + d) * L.ty + b) * boxx + a + kTmaX0 - 1];
+            const int row = i / L.tx, a = i - row * L.tx;
+            ebd[i] = (EB)src[row * boxx + a];
         }
     } else if (!SPLIT) {
         // flat over (component, z, y, x) so every lane works, and batches of

@@ -1,0 +1,9 @@
+# TMA issued at kernel entry + division-free widen: parity subset, A/B vs the previous build (early + steady)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dense.py tests/test_gpu_random.py tests/test_gpu_edges.py tests/test_gpu_scale.py -q -m gpu --timeout 900 > gpurun_out/pytest_r02u.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_r02u.log
+L=paper_1606_02862_b200/libkwb200.so
+timeout 1500 python tools/ab.py --config c2 --rounds 3 --steps 20 --warmup 5 exp/libkwb200_base.so $L > gpurun_out/ab_r02u_early.txt 2>&1
+timeout 1500 python tools/ab.py --config c2 --rounds 2 --steps 20 --warmup 40 exp/libkwb200_base.so $L > gpurun_out/ab_r02u_steady.txt 2>&1
+echo done
