@@ -51,6 +51,55 @@ def test_library_rejects_bad_arguments_without_gpu():
     assert rc == -1
 
 
+def test_species_entry_points_reject_bad_arguments_without_gpu():
+    """kwb_particles_advance_species / _split validate the species count,
+    the shape order and every store (workspace included) before any launch
+    (fake device pointers: nothing may reach the GPU)."""
+    from paper_1606_02862_b200 import _lib
+    lib = _lib.load()
+    g = _lib.Grid(nx=16, ny=16, nz=8, scx=8, scy=8, scz=4, gx=2, gy=2, gz=2, dtype=0,
+                  dx=1.0, dy=1.0, dz=1.0, dt=0.5)
+    fake = 0x10000
+
+    def store(frames):
+        st = _lib.StoreC()
+        for c in ("ox", "oy", "oz", "ux", "uy", "uz", "w", "front", "back"):
+            setattr(st, c, fake)
+        st.frames_per_sc = frames
+        return st
+    ex = _lib.ExchangeC()
+    for c in ("ox", "oy", "oz", "ux", "uy", "uz", "w", "cx", "cy", "cz", "dest", "count"):
+        setattr(ex, c, fake)
+    ex.capacity = 16
+    sp = (_lib.SpeciesC * 5)()
+    ins = (_lib.StoreC * 5)(*[store(8) for _ in range(5)])
+    outs = (_lib.StoreC * 5)(*[store(8) for _ in range(5)])
+    ptr = _lib.Ptr3(fake, fake, fake)
+    status = fake
+    call = lambda name, *a: getattr(lib, name)(ctypes.byref(g), *a)
+    # five species: more than kMaxSpecies
+    rc = call("kwb_particles_advance_species", 5, sp, ins, outs, ctypes.byref(ex), ptr, ptr, ptr,
+              None, 2, status, None)
+    assert rc == -1 and b"at most" in lib.kwb_last_error()
+    # split: a workspace store of another frame count
+    wss = (_lib.StoreC * 2)(store(8), store(9))
+    rc = call("kwb_particles_advance_split", 2, sp, ins, outs, wss, ctypes.byref(ex), ptr, ptr,
+              ptr, None, 2, status, None)
+    assert rc == -1 and b"frames_per_sc" in lib.kwb_last_error()
+    # split: an incomplete workspace store
+    bad = store(8)
+    bad.w = None
+    wss = (_lib.StoreC * 2)(store(8), bad)
+    rc = call("kwb_particles_advance_split", 2, sp, ins, outs, wss, ctypes.byref(ex), ptr, ptr,
+              ptr, None, 1, status, None)
+    assert rc == -1 and b"workspace" in lib.kwb_last_error()
+    # split: unknown shape order
+    wss = (_lib.StoreC * 2)(store(8), store(8))
+    rc = call("kwb_particles_advance_split", 2, sp, ins, outs, wss, ctypes.byref(ex), ptr, ptr,
+              ptr, None, 5, status, None)
+    assert rc == -1 and b"shape_order" in lib.kwb_last_error()
+
+
 def test_simparams_validation():
     from paper_1606_02862_b200.pic import SimParams, default_species
     with pytest.raises(ValueError):
