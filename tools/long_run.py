@@ -32,12 +32,15 @@ def main():
             sim.enqueue_step()
         e1.record()
         torch.cuda.synchronize()
-        sim.check_status()
+        st = sim.check_status()
         done += a.every
         d = sim.diagnostics()
+        from paper_1606_02862_b200 import _lib
+        leavers = int(st[:, _lib.ST_LEAVERS].max())   # the last step's super-cell leavers
         print(f"step {done:6d}: {e0.elapsed_time(e1) / a.every:7.3f} ms/step, frames "
-              f"{[st.frames_per_sc for st in sim.stores]}, census {sim.census() - n0:+d}, "
-              f"field energy {d['field_energy']:.4e}, KE {d['kinetic_energy']:.6e}", flush=True)
+              f"{[st_.frames_per_sc for st_ in sim.stores]}, census {sim.census() - n0:+d}, "
+              f"leavers {leavers}, field energy {d['field_energy']:.4e}, "
+              f"KE {d['kinetic_energy']:.6e}", flush=True)
 
 
 if __name__ == "__main__":
