@@ -76,3 +76,13 @@ def test_split_contract_violation(dtype, monkeypatch):
     sim.load_state(particles=[pk])
     with pytest.raises(ContractViolation, match="1 particle"):
         sim.step()
+
+
+@pytest.mark.parametrize("fuse_j", [False, True])
+def test_split_in_zslab_decomposition(fuse_j, monkeypatch):
+    """The split advance under the z-slab decomposition (two loopback slabs,
+    message or fused J halo) against the single domain, as
+    test_gpu_decomp.py checks the fused advance."""
+    monkeypatch.setenv("KWB_SPLIT", "1")
+    from test_gpu_decomp import test_loopback_slabs_match_single_domain
+    test_loopback_slabs_match_single_domain(2, np.float32, "tsc", fuse_j)
